@@ -1,0 +1,535 @@
+// C ABI, device half: Executor, bound (HBM-resident) plans, the host-span
+// run_spmv / run_sptrsv contracts, execute_plan and exec_*_codelet.
+//
+// Reference: /root/reference/proj/core/src/executor.cpp:252-308 (Executor,
+// execute_plan, run_spmv, run_sptrsv) and :53-116 (exec_*_codelet).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "capi_types.hpp"
+#include "common.hpp"
+#include "kernels.hpp"
+#include "lower.hpp"
+
+using namespace pscb;
+
+namespace pscb {
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owned device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t n) {
+        if (n <= bytes && p) return;
+        release();
+        ck(cudaMalloc(&p, std::max<size_t>(n, 16)), "cudaMalloc");
+        bytes = std::max<size_t>(n, 16);
+    }
+    template <class T>
+    void upload(const std::vector<T>& v, cudaStream_t s) {
+        ensure(v.size() * sizeof(T));
+        if (!v.empty()) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    }
+    void upload_raw(const void* h, size_t n, cudaStream_t s) {
+        ensure(n);
+        if (n) ck(cudaMemcpyAsync(p, h, n, cudaMemcpyHostToDevice, s), "H2D");
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace pscb
+
+struct psc_bound {
+    int device = 0;
+    int kernel = PSC_KERNEL_SPMV;
+    int mode = PSC_MODE_PARITY;
+    int32_t row_begin = 0, row_end = 0, n_rows_total = 0, n_cols = 0;
+    int64_t k_begin = 0, k_end = 0;
+    bool canonical = true, simple = true;
+    int n_chunks = 0, n_blocks = 0, max_block_rows = 0;
+    int64_t n_segments = 0, long_rows = 0;
+    std::string why_general;
+    DevBuf ro, col, val;
+    DevBuf rsp, sst, slen, svec, chunk_row, ticket, armed;
+    int32_t epoch = 0;      // per-launch arming epoch of the solve kernel
+    DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
+    // general path
+    std::vector<int64_t> part_group_ptr;
+    DevBuf g_cp, g_fp, g_kind, g_m, g_n, g_form, g_base, g_so, g_si, g_tab, g_tables, g_frow, g_fdiag, g_frhs;
+    // host-side fingerprint used by the run_* cache
+    std::vector<int32_t> finger;
+
+    int32_t rows() const { return row_end - row_begin; }
+    SegmentsDev segs() const {
+        if (simple) return {};
+        return {rsp.as<int32_t>(), sst.as<int32_t>(), slen.as<int32_t>(), svec.as<int32_t>()};
+    }
+    GeneralDev gen() const {
+        return {g_cp.as<int64_t>(),  g_fp.as<int64_t>(),  g_kind.as<int32_t>(), g_m.as<int32_t>(),
+                g_n.as<int32_t>(),   g_form.as<int32_t>(), g_base.as<int32_t>(), g_so.as<int32_t>(),
+                g_si.as<int32_t>(),  g_tab.as<int64_t>(),  g_tables.as<int32_t>(), g_frow.as<int32_t>(),
+                g_fdiag.as<int32_t>(), g_frhs.as<int32_t>()};
+    }
+    int64_t algorithmic_bytes() const {
+        int64_t nnz = k_end - k_begin, r = rows();
+        if (kernel == PSC_KERNEL_SPMV) return 12 * nnz + 4 * (r + 1) + 8LL * n_cols + 8 * r;
+        return 12 * nnz + 4 * (r + 1) + 16 * r;
+    }
+    int64_t device_bytes() const {
+        size_t t = 0;
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &ticket, &armed, &g_cp, &g_fp,
+                                &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
+                                &g_fdiag, &g_frhs})
+            t += b->bytes;
+        return static_cast<int64_t>(t);
+    }
+};
+
+struct psc_executor {
+    int workers = 1;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    // run_* cache: (plan serial, structure pointers, sizes, general flag) -> bound
+    std::map<std::tuple<uint64_t, const void*, const void*, int64_t, int32_t, int>, std::unique_ptr<psc_bound>> cache;
+    DevBuf vx, vy, vb, vacc;
+};
+
+namespace pscb {
+namespace {
+
+void use_device(int device) { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+std::vector<int32_t> fingerprint(const psc_csr_view& a) {
+    std::vector<int32_t> f;
+    const int samples = 64;
+    for (int i = 0; i < samples && a.n_rows > 0; ++i) f.push_back(a.row_offsets[(static_cast<int64_t>(a.n_rows) * i) / samples]);
+    for (int i = 0; i < samples && a.nnz > 0; ++i) f.push_back(a.col_indices[(a.nnz * i) / samples]);
+    return f;
+}
+
+// Build a bound plan. force_general lowers through the exact interpreter
+// (execute_plan semantics need accumulate-onto-existing for the solve).
+std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_view& a, int mode, int64_t p0,
+                                      int64_t p1, bool force_general, cudaStream_t s) {
+    if (p.kernel == PSC_KERNEL_SPTRSV) adopt_triangular(a);
+    else validate_csr(a);
+    Lowered L = lower_plan(p, a, p0, p1, 0, force_general);
+    auto b = std::make_unique<psc_bound>();
+    b->device = device;
+    b->kernel = p.kernel;
+    b->mode = mode;
+    b->row_begin = L.row_begin;
+    b->row_end = L.row_end;
+    b->n_rows_total = a.n_rows;
+    b->n_cols = a.n_cols;
+    b->k_begin = L.k_begin;
+    b->k_end = L.k_end;
+    b->canonical = L.canonical;
+    b->simple = L.simple;
+    b->why_general = L.why_general;
+    b->finger = fingerprint(a);
+    use_device(device);
+    if (L.canonical) {
+        const int32_t nr = b->rows();
+        std::vector<int32_t> ro(static_cast<size_t>(nr) + 1);
+        for (int32_t r = 0; r <= nr; ++r) ro[r] = static_cast<int32_t>(a.row_offsets[r + L.row_begin] - L.k_begin);
+        b->ro.upload(ro, s);
+        b->col.upload_raw(a.col_indices + L.k_begin, (L.k_end - L.k_begin) * sizeof(int32_t), s);
+        b->val.upload_raw(a.values + L.k_begin, (L.k_end - L.k_begin) * sizeof(double), s);
+        if (!L.simple) {
+            b->rsp.upload(L.row_seg_ptr, s);
+            b->sst.upload(L.seg_start, s);
+            b->slen.upload(L.seg_len, s);
+            b->svec.upload(L.seg_vec, s);
+            b->n_segments = static_cast<int64_t>(L.seg_start.size());
+        }
+        if (p.kernel == PSC_KERNEL_SPMV) {
+            b->chunk_row.upload(L.chunk_row, s);
+            b->n_chunks = static_cast<int>(L.chunk_row.size()) - 1;
+            b->long_rows = L.long_rows;
+        } else {
+            b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
+            b->max_block_rows = L.max_block_rows;
+            b->ticket.ensure(2 * sizeof(int32_t));
+            ck(cudaMemsetAsync(b->ticket.p, 0, 2 * sizeof(int32_t), s), "memset");
+            b->armed.ensure(std::max(1, b->n_blocks) * sizeof(int32_t));
+            ck(cudaMemsetAsync(b->armed.p, 0, std::max(1, b->n_blocks) * sizeof(int32_t), s), "memset");
+        }
+    } else {
+        // general interpreter: full CSR values, descriptors and tables
+        b->val.upload_raw(a.values, a.nnz * sizeof(double), s);
+        auto& G = L.gen;
+        b->part_group_ptr = G.part_group_ptr;
+        b->g_cp.upload(G.group_codelet_ptr, s);
+        b->g_fp.upload(G.group_fin_ptr, s);
+        b->g_kind.upload(G.c_kind, s);
+        b->g_m.upload(G.c_m, s);
+        b->g_n.upload(G.c_n, s);
+        b->g_form.upload(G.d_form, s);
+        b->g_base.upload(G.d_base, s);
+        b->g_so.upload(G.d_so, s);
+        b->g_si.upload(G.d_si, s);
+        b->g_tab.upload(G.d_tab, s);
+        b->g_tables.upload(G.tables, s);
+        b->g_frow.upload(G.f_row, s);
+        b->g_fdiag.upload(G.f_diag, s);
+        b->g_frhs.upload(G.f_rhs, s);
+    }
+    ck(cudaStreamSynchronize(s), "bind sync");
+    return b;
+}
+
+void run_general(psc_bound* b, const double* gather, double* accum, const double* rhs, double* solution,
+                 cudaStream_t s) {
+    GeneralDev g = b->gen();
+    for (size_t p = 0; p + 1 < b->part_group_ptr.size(); ++p) {
+        launch_general_partition(g, b->part_group_ptr[p], b->part_group_ptr[p + 1], b->val.as<double>(), gather, accum,
+                                 rhs, solution, s);
+    }
+    ck(cudaGetLastError(), "general kernel launch");
+}
+
+void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
+    use_device(b->device);
+    if (b->canonical) {
+        launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
+                           b->chunk_row.as<int32_t>(), b->n_chunks, b->segs(), false, s);
+    } else {
+        ck(cudaMemsetAsync(y, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset y");
+        run_general(b, x, y, nullptr, nullptr, s);
+    }
+    ck(cudaGetLastError(), "spmv launch");
+}
+
+void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s) {
+    use_device(b->device);
+    if (b->canonical) {
+        b->epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;
+        launch_sptrsv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc, b->rows(),
+                             b->max_block_rows, b->segs(), b->ticket.as<int32_t>(), b->armed.as<int32_t>(), b->epoch,
+                             s);
+    } else {
+        require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
+        ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");
+        run_general(b, x, acc, rhs, x, s);
+    }
+    ck(cudaGetLastError(), "sptrsv launch");
+}
+
+psc_bound* cached_bound(psc_executor* e, const psc_plan* plan, const psc_csr_view& a, bool general) {
+    auto key = std::make_tuple(plan->serial, static_cast<const void*>(a.row_offsets),
+                               static_cast<const void*>(a.col_indices), a.nnz, a.n_rows, general ? 1 : 0);
+    auto it = e->cache.find(key);
+    if (it != e->cache.end() && it->second->finger == fingerprint(a)) return it->second.get();
+    auto b = make_bound(e->device, plan->p, a, PSC_MODE_PARITY, -1, -1, general, e->stream);
+    psc_bound* raw = b.get();
+    e->cache[key] = std::move(b);
+    return raw;
+}
+
+}  // namespace
+}  // namespace pscb
+
+extern "C" {
+
+PSC_API int32_t psc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+PSC_API psc_status psc_executor_create(int32_t workers, int32_t device, psc_executor** out) {
+    return guarded([&] {
+        require(out != nullptr, "Executor: null output");
+        if (workers < 1) throw std::invalid_argument("Executor: worker count must be >= 1");
+        int n = psc_device_count();
+        if (n <= 0) throw CudaError("Executor: no CUDA device is available");
+        require(device >= 0 && device < n, "Executor: device index out of range");
+        auto e = std::make_unique<psc_executor>();
+        e->workers = workers;
+        e->device = device;
+        use_device(device);
+        ck(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        *out = e.release();
+    });
+}
+PSC_API int32_t psc_executor_workers(const psc_executor* e) { return e ? e->workers : 0; }
+PSC_API void psc_executor_destroy(psc_executor* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    e->cache.clear();
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+}
+
+PSC_API psc_status psc_bind(psc_executor* e, const psc_plan* plan, const psc_csr_view* a, int32_t mode,
+                            psc_bound** out) {
+    return guarded([&] {
+        require(e && plan && a && out, "bind: null argument");
+        require(mode == PSC_MODE_PARITY || mode == PSC_MODE_FAST, "bind: unknown mode");
+        std::lock_guard<std::mutex> lk(e->mu);
+        *out = make_bound(e->device, plan->p, *a, mode, -1, -1, false, e->stream).release();
+    });
+}
+PSC_API psc_status psc_bind_partitions(psc_executor* e, const psc_plan* plan, const psc_csr_view* a, int32_t mode,
+                                       int64_t part_begin, int64_t part_end, psc_bound** out) {
+    return guarded([&] {
+        require(e && plan && a && out, "bind_partitions: null argument");
+        require(part_end >= 0, "bind_partitions: part_end must be >= 0");
+        std::lock_guard<std::mutex> lk(e->mu);
+        *out = make_bound(e->device, plan->p, *a, mode, part_begin, part_end, false, e->stream).release();
+    });
+}
+PSC_API psc_status psc_bound_rows(const psc_bound* b, int32_t* row_begin, int32_t* row_end) {
+    return guarded([&] {
+        require(b != nullptr, "bound: null");
+        if (row_begin) *row_begin = b->row_begin;
+        if (row_end) *row_end = b->row_end;
+    });
+}
+PSC_API void psc_bound_destroy(psc_bound* b) {
+    if (!b) return;
+    cudaSetDevice(b->device);
+    delete b;
+}
+PSC_API psc_status psc_bound_spmv(psc_bound* b, const double* x, double* y, void* stream) {
+    return guarded([&] {
+        require(b && x && y, "spmv: null argument");
+        require(b->kernel == PSC_KERNEL_SPMV, "run_spmv: plan was built for another kernel");
+        bound_spmv(b, x, y, static_cast<cudaStream_t>(stream));
+    });
+}
+PSC_API psc_status psc_bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, void* stream) {
+    return guarded([&] {
+        require(b && rhs && x, "sptrsv: null argument");
+        require(b->kernel == PSC_KERNEL_SPTRSV, "run_sptrsv: plan was built for another kernel");
+        bound_sptrsv(b, rhs, x, acc, static_cast<cudaStream_t>(stream));
+    });
+}
+// Host-buffer variants (the e2e path): H2D of the input, the kernel and the
+// D2H of the result, all enqueued on `stream`. Host memory should be pinned
+// for the copies to be asynchronous.
+PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x, double* y, void* stream) {
+    return guarded([&] {
+        require(b && x && y, "spmv_host: null argument");
+        require(b->kernel == PSC_KERNEL_SPMV, "run_spmv: plan was built for another kernel");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        use_device(b->device);
+        b->hx.upload_raw(x, static_cast<size_t>(b->n_cols) * sizeof(double), s);
+        b->hy.ensure(std::max(1, b->rows()) * sizeof(double));
+        bound_spmv(b, b->hx.as<double>(), b->hy.as<double>(), s);
+        ck(cudaMemcpyAsync(y, b->hy.p, static_cast<size_t>(b->rows()) * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    });
+}
+PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double* x, double* acc, void* stream) {
+    return guarded([&] {
+        require(b && rhs && x, "sptrsv_host: null argument");
+        require(b->kernel == PSC_KERNEL_SPTRSV, "run_sptrsv: plan was built for another kernel");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        use_device(b->device);
+        const size_t bytes = static_cast<size_t>(b->rows()) * sizeof(double);
+        b->hy.upload_raw(rhs, bytes, s);
+        b->hx.ensure(std::max<size_t>(bytes, 8));
+        if (!b->canonical) b->hx.upload_raw(x, bytes, s);
+        if (acc || !b->canonical) b->hacc.ensure(std::max<size_t>(bytes, 8));
+        bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), (acc || !b->canonical) ? b->hacc.as<double>() : nullptr, s);
+        ck(cudaMemcpyAsync(x, b->hx.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+        if (acc) ck(cudaMemcpyAsync(acc, b->hacc.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    });
+}
+PSC_API int32_t psc_bound_launches(const psc_bound* b) {
+    if (!b) return 0;
+    if (b->canonical) return 1;
+    return static_cast<int32_t>(b->part_group_ptr.size()) - 1;
+}
+PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]) {
+    return guarded([&] {
+        require(b && out, "bound_info: null argument");
+        out[0] = b->rows();
+        out[1] = b->canonical ? b->n_segments : -1;
+        out[2] = b->kernel == PSC_KERNEL_SPMV ? b->n_chunks : b->n_blocks;
+        out[3] = b->canonical ? 0 : 1;
+        out[4] = b->algorithmic_bytes();
+        out[5] = b->device_bytes();
+        out[6] = b->long_rows;
+        out[7] = b->max_block_rows;
+    });
+}
+
+PSC_API psc_status psc_csr_spmv_device(const psc_bound* b, const double* x, double* y, void* stream) {
+    return guarded([&] {
+        require(b && x && y, "csr_spmv: null argument");
+        require(b->canonical, "csr_spmv: needs a canonical bound plan");
+        use_device(b->device);
+        launch_csr_spmv_naive(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y, b->rows(),
+                              static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "csr_spmv launch");
+    });
+}
+
+// run_spmv, executor.cpp:274-288.
+PSC_API psc_status psc_run_spmv(psc_executor* e, const psc_plan* plan, const psc_csr_view* a, const double* x,
+                                int64_t nx, double* y, int64_t ny) {
+    return guarded([&] {
+        require(e && plan && a, "run_spmv: null argument");
+        if (plan->p.kernel != PSC_KERNEL_SPMV) throw std::invalid_argument("run_spmv: plan was built for another kernel");
+        if (nx != a->n_cols || ny != a->n_rows) throw std::invalid_argument("run_spmv: vector size mismatch");
+        std::lock_guard<std::mutex> lk(e->mu);
+        psc_bound* b = cached_bound(e, plan, *a, false);
+        cudaStream_t s = e->stream;
+        use_device(e->device);
+        b->val.upload_raw(a->values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);  // values may change
+        e->vx.upload_raw(x, nx * sizeof(double), s);
+        e->vy.ensure(std::max<int64_t>(ny, 1) * sizeof(double));
+        bound_spmv(b, e->vx.as<double>(), e->vy.as<double>(), s);
+        if (ny) ck(cudaMemcpyAsync(y, e->vy.p, ny * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "run_spmv sync");
+    });
+}
+
+// run_sptrsv, executor.cpp:290-308.
+PSC_API psc_status psc_run_sptrsv(psc_executor* e, const psc_plan* plan, const psc_csr_view* l, const double* rhs,
+                                  int64_t nb, double* x, int64_t nx, double* acc, int64_t nacc) {
+    return guarded([&] {
+        require(e && plan && l, "run_sptrsv: null argument");
+        if (plan->p.kernel != PSC_KERNEL_SPTRSV)
+            throw std::invalid_argument("run_sptrsv: plan was built for another kernel");
+        int64_t n = l->n_rows;
+        if (nb != n || nx != n || nacc != n) throw std::invalid_argument("run_sptrsv: vector size mismatch");
+        std::lock_guard<std::mutex> lk(e->mu);
+        psc_bound* b = cached_bound(e, plan, *l, false);
+        cudaStream_t s = e->stream;
+        use_device(e->device);
+        b->val.upload_raw(l->values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);
+        size_t bytes = std::max<int64_t>(n, 1) * sizeof(double);
+        e->vb.upload_raw(rhs, n * sizeof(double), s);
+        e->vx.ensure(bytes);
+        e->vacc.ensure(bytes);
+        if (!b->canonical && n) e->vx.upload_raw(x, n * sizeof(double), s);  // stale reads see caller's x
+        bound_sptrsv(b, e->vb.as<double>(), e->vx.as<double>(), e->vacc.as<double>(), s);
+        if (n) {
+            ck(cudaMemcpyAsync(x, e->vx.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H x");
+            if (acc) ck(cudaMemcpyAsync(acc, e->vacc.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H acc");
+        }
+        ck(cudaStreamSynchronize(s), "run_sptrsv sync");
+    });
+}
+
+// execute_plan, executor.cpp:269-272: no zero-fill, accumulate onto ctx.
+PSC_API psc_status psc_execute_plan(psc_executor* e, const psc_plan* plan, const psc_csr_view* a,
+                                    const psc_exec_context* ctx) {
+    return guarded([&] {
+        require(e && plan && a && ctx, "execute_plan: null argument");
+        require(ctx->matrix_values && ctx->gather && ctx->accum, "execute_plan: null context array");
+        const bool solve = ctx->rhs != nullptr;
+        if (solve) require(ctx->solution != nullptr, "execute_plan: solve context needs a solution array");
+        std::lock_guard<std::mutex> lk(e->mu);
+        psc_bound* b = cached_bound(e, plan, *a, true);
+        cudaStream_t s = e->stream;
+        use_device(e->device);
+        const int64_t n = a->n_rows, nc = a->n_cols;
+        b->val.upload_raw(ctx->matrix_values, a->nnz * sizeof(double), s);
+        e->vy.upload_raw(ctx->accum, n * sizeof(double), s);
+        if (solve) {
+            // gather aliases solution (executor.hpp:12-23)
+            e->vx.upload_raw(ctx->solution, n * sizeof(double), s);
+            e->vb.upload_raw(ctx->rhs, n * sizeof(double), s);
+            run_general(b, e->vx.as<double>(), e->vy.as<double>(), e->vb.as<double>(), e->vx.as<double>(), s);
+            if (n) ck(cudaMemcpyAsync(ctx->solution, e->vx.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        } else {
+            e->vx.upload_raw(ctx->gather, nc * sizeof(double), s);
+            run_general(b, e->vx.as<double>(), e->vy.as<double>(), nullptr, nullptr, s);
+        }
+        if (n) ck(cudaMemcpyAsync(ctx->accum, e->vy.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "execute_plan sync");
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+psc_status exec_one(int which, const psc_codelet_view* c, const psc_exec_context* ctx) {
+    return guarded([&] {
+        require(c && ctx, "exec_codelet: null argument");
+        Lowered L = lower_single_codelet(*c, which);
+        const auto& G = L.gen;
+        int n = psc_device_count();
+        if (n <= 0) throw CudaError("exec_codelet: no CUDA device is available");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        psc_bound b;
+        b.device = dev;
+        b.canonical = false;
+        cudaStream_t s = nullptr;
+        b.part_group_ptr = G.part_group_ptr;
+        b.g_cp.upload(G.group_codelet_ptr, s);
+        b.g_fp.upload(G.group_fin_ptr, s);
+        b.g_kind.upload(G.c_kind, s);
+        b.g_m.upload(G.c_m, s);
+        b.g_n.upload(G.c_n, s);
+        b.g_form.upload(G.d_form, s);
+        b.g_base.upload(G.d_base, s);
+        b.g_so.upload(G.d_so, s);
+        b.g_si.upload(G.d_si, s);
+        b.g_tab.upload(G.d_tab, s);
+        b.g_tables.upload(G.tables, s);
+        b.g_frow.upload(G.f_row, s);
+        b.g_fdiag.upload(G.f_diag, s);
+        b.g_frhs.upload(G.f_rhs, s);
+        const int64_t nm = G.max_mat + 1, nv = G.max_vec + 1, no = G.max_out + 1;
+        if (nm > 0) require(ctx->matrix_values != nullptr, "exec_codelet: null matrix_values");
+        if (nv > 0) require(ctx->gather != nullptr, "exec_codelet: null gather");
+        if (no > 0) require(ctx->accum != nullptr, "exec_codelet: null accum");
+        b.val.upload_raw(ctx->matrix_values, std::max<int64_t>(nm, 0) * sizeof(double), s);
+        DevBuf g, acc, rhs_flag;
+        g.upload_raw(ctx->gather, std::max<int64_t>(nv, 0) * sizeof(double), s);
+        acc.upload_raw(ctx->accum, std::max<int64_t>(no, 0) * sizeof(double), s);
+        rhs_flag.ensure(sizeof(double));
+        run_general(&b, g.as<double>(), acc.as<double>(), ctx->rhs ? rhs_flag.as<double>() : nullptr, nullptr, s);
+        if (no > 0) ck(cudaMemcpyAsync(ctx->accum, acc.p, no * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "exec_codelet sync");
+    });
+}
+
+}  // namespace
+
+extern "C" {
+PSC_API psc_status psc_exec_blas_codelet(const psc_codelet_view* c, const psc_exec_context* ctx) {
+    return exec_one(PSC_CODELET_BLAS, c, ctx);
+}
+PSC_API psc_status psc_exec_psci_codelet(const psc_codelet_view* c, const psc_exec_context* ctx) {
+    return exec_one(PSC_CODELET_PSC_I, c, ctx);
+}
+PSC_API psc_status psc_exec_pscii_codelet(const psc_codelet_view* c, const psc_exec_context* ctx) {
+    return exec_one(PSC_CODELET_PSC_II, c, ctx);
+}
+}

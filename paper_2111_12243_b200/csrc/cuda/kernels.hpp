@@ -1,0 +1,59 @@
+// Launch wrappers for the sm_100a kernels (definitions in kernels.cu).
+// Rows and CSR positions are local to the bound row range: ro[] is rebased
+// so ro[0] == 0, col/val hold only the bound rows' entries, y holds only the
+// bound rows; x (the gathered vector) is always the full vector.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pscb {
+
+struct SegmentsDev {
+    const int32_t* row_seg_ptr = nullptr;  // null => every row is one implicit full-row segment
+    const int32_t* seg_start = nullptr;
+    const int32_t* seg_len = nullptr;
+    const int32_t* seg_vec = nullptr;
+};
+
+// y[r] = (accumulate ? y[r] : 0) + sum of row r's segment partials in plan
+// order, each a 4-lane dot (executor.cpp:23-49). One CTA per chunk.
+void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
+                        double* y, const int32_t* chunk_row, int n_chunks, SegmentsDev segs,
+                        bool accumulate, cudaStream_t stream);
+
+// Sync-free blocked triangular solve over uniform row blocks of block_rows
+// rows. ticket: 2 zeroed ints, left zeroed on exit; armed: one int per block,
+// epoch must differ from every value armed[] holds (a per-launch counter).
+void launch_sptrsv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* b,
+                          double* x, double* acc_out, int n_rows, int block_rows, SegmentsDev segs,
+                          int32_t* ticket, int32_t* armed, int epoch, cudaStream_t stream);
+
+// General interpreter (exact Listing-3 semantics) over groups [g0, g1) of one
+// partition; one thread per region group.
+struct GeneralDev {
+    const int64_t* group_codelet_ptr;
+    const int64_t* group_fin_ptr;
+    const int32_t* c_kind;
+    const int32_t* c_m;
+    const int32_t* c_n;
+    const int32_t* d_form;
+    const int32_t* d_base;
+    const int32_t* d_so;
+    const int32_t* d_si;
+    const int64_t* d_tab;
+    const int32_t* tables;
+    const int32_t* f_row;
+    const int32_t* f_diag;
+    const int32_t* f_rhs;
+};
+void launch_general_partition(GeneralDev g, int64_t g0, int64_t g1, const double* matrix_values,
+                              const double* gather, double* accum, const double* rhs, double* solution,
+                              cudaStream_t stream);
+
+// Naive row-sequential CSR SpMV (spmv_csr_baseline, executor.cpp:310-323).
+void launch_csr_spmv_naive(const int32_t* ro, const int32_t* col, const double* val, const double* x,
+                           double* y, int32_t n_rows, cudaStream_t stream);
+
+}  // namespace pscb

@@ -1,0 +1,416 @@
+// Plan -> device layout lowering (see lower.hpp).
+#include "lower.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.hpp"
+
+namespace pscb {
+
+void check_codelet_shape(int which, int out_form, int mat_form, int vec_form) {
+    bool ot = out_form != PSC_FORM_STRIDED, mt = mat_form != PSC_FORM_STRIDED, vt = vec_form != PSC_FORM_STRIDED;
+    if (which == PSC_CODELET_BLAS) {
+        if (ot || mt || vt) throw std::invalid_argument("exec_blas_codelet: descriptors must be strided");
+    } else if (which == PSC_CODELET_PSC_I) {
+        if (ot || mt || !vt) throw std::invalid_argument("exec_psci_codelet: expects one gather table");
+    } else {
+        if (!ot || mt || !vt) throw std::invalid_argument("exec_pscii_codelet: expects output and gather tables");
+    }
+}
+
+namespace {
+
+int dispatch_kind(int kind) {  // exec_codelet switch, executor.cpp:120-126
+    return kind == PSC_CODELET_BLAS ? PSC_CODELET_BLAS : kind == PSC_CODELET_PSC_I ? PSC_CODELET_PSC_I : PSC_CODELET_PSC_II;
+}
+
+struct SegRec {
+    int32_t row;  // local
+    int32_t start, len, vec;
+};
+
+// Table entry e of descriptor d of codelet c, bounds-checked.
+int64_t tab_at(const Plan& p, const DescView& v, int64_t c, int d, int64_t e, const psc_csr_view& a) {
+    if (e >= v.len) throw std::invalid_argument("codelet: table shorter than the codelet extent");
+    return v.tab ? v.tab[e] : p.implicit_entry(c, d, e, a.row_offsets, a.col_indices);
+}
+
+void build_general(const Plan& p, const psc_csr_view& a, Lowered& L) {
+    auto& G = L.gen;
+    const int64_t C = p.n_codelets();
+    G.part_group_ptr = p.part_group_ptr;
+    G.group_codelet_ptr = p.g_codelet_ptr;
+    G.c_kind.resize(C);
+    G.c_m.resize(C);
+    G.c_n.resize(C);
+    G.d_form.resize(3 * C);
+    G.d_base.resize(3 * C);
+    G.d_so.resize(3 * C);
+    G.d_si.resize(3 * C);
+    G.d_tab.resize(3 * C);
+    for (int64_t c = 0; c < C; ++c) {
+        const int which = dispatch_kind(p.c_kind[c]);
+        const int m = p.c_m[c], n = p.c_n[c];
+        G.c_kind[c] = which;
+        G.c_m[c] = m;
+        G.c_n[c] = n;
+        DescView ds[3] = {p.desc(c, 0), p.desc(c, 1), p.desc(c, 2)};
+        check_codelet_shape(which, ds[0].form, ds[1].form, ds[2].form);
+        for (int d = 0; d < 3; ++d) {
+            G.d_form[3 * c + d] = ds[d].form;
+            G.d_base[3 * c + d] = ds[d].base;
+            G.d_so[3 * c + d] = ds[d].so;
+            G.d_si[3 * c + d] = ds[d].si;
+            G.d_tab[3 * c + d] = static_cast<int64_t>(G.tables.size());
+            if (ds[d].form != PSC_FORM_STRIDED) {
+                for (int64_t e = 0; e < ds[d].len; ++e) G.tables.push_back(static_cast<int32_t>(tab_at(p, ds[d], c, d, e, a)));
+            }
+        }
+        if (m <= 0 || n <= 0) continue;  // the reference loops do nothing
+        // Index ranges the executor will touch (exec_* semantics).
+        auto lin = [&](int d, int64_t i, int64_t j) {
+            return static_cast<int64_t>(ds[d].base) + i * ds[d].so + j * ds[d].si;
+        };
+        auto track = [](int64_t& mx, int64_t v) {
+            if (v < 0) throw std::invalid_argument("codelet: negative index");
+            mx = std::max(mx, v);
+        };
+        for (int64_t i : {int64_t(0), int64_t(m - 1)})
+            for (int64_t j : {int64_t(0), int64_t(n - 1)}) track(G.max_mat, lin(1, i, j));
+        if (which == PSC_CODELET_BLAS) {
+            for (int64_t i : {int64_t(0), int64_t(m - 1)}) {
+                track(G.max_out, lin(0, i, 0));
+                for (int64_t j : {int64_t(0), int64_t(n - 1)}) track(G.max_vec, lin(2, i, j));
+            }
+        } else {
+            if (which == PSC_CODELET_PSC_I) {
+                for (int64_t i : {int64_t(0), int64_t(m - 1)}) track(G.max_out, lin(0, i, 0));
+            } else {
+                for (int64_t i = 0; i < m; ++i) track(G.max_out, tab_at(p, ds[0], c, 0, i, a));
+            }
+            bool per_point = which == PSC_CODELET_PSC_II && ds[2].form == PSC_FORM_POINT_TABLE;
+            int64_t cnt = per_point ? static_cast<int64_t>(m) * n : n;
+            for (int64_t e = 0; e < cnt; ++e) track(G.max_vec, tab_at(p, ds[2], c, 2, e, a));
+        }
+    }
+    // finalize records
+    G.group_fin_ptr.assign(p.n_groups() + 1, 0);
+    for (int64_t g = 0; g < p.n_groups(); ++g) {
+        if (!p.mined) {
+            for (int64_t f = p.g_fin_ptr[g]; f < p.g_fin_ptr[g + 1]; ++f) {
+                G.f_row.push_back(p.f_row[f]);
+                G.f_diag.push_back(p.f_diag[f]);
+                G.f_rhs.push_back(p.f_rhs[f]);
+            }
+        } else if (p.kernel == PSC_KERNEL_SPTRSV) {
+            for (int32_t r = p.g_row_begin[g]; r < p.g_row_end[g]; ++r) {
+                G.f_row.push_back(r);
+                G.f_diag.push_back(a.row_offsets[r + 1] - 1);
+                G.f_rhs.push_back(r);
+            }
+        }
+        G.group_fin_ptr[g + 1] = static_cast<int64_t>(G.f_row.size());
+    }
+    for (std::size_t f = 0; f < G.f_row.size(); ++f) {
+        if (G.f_row[f] < 0 || G.f_row[f] >= a.n_rows || G.f_rhs[f] < 0 || G.f_rhs[f] >= a.n_rows ||
+            G.f_diag[f] < 0 || G.f_diag[f] >= a.nnz)
+            throw std::invalid_argument("finalize record index out of range");
+    }
+    if (G.max_mat >= a.nnz) throw std::invalid_argument("codelet: matrix index out of range");
+    if (G.max_vec >= a.n_cols) throw std::invalid_argument("codelet: gather index out of range");
+    if (G.max_out >= a.n_rows) throw std::invalid_argument("codelet: output index out of range");
+}
+
+}  // namespace
+
+Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int64_t part_end,
+                   int sptrsv_block_rows, bool force_general) {
+    require(p.n_rows == a.n_rows && p.n_cols == a.n_cols && p.nnz == a.nnz,
+            "bind: matrix does not match the plan");
+    const int32_t* ro = a.row_offsets;
+    const int sp = p.kernel == PSC_KERNEL_SPTRSV ? 1 : 0;
+    Lowered L;
+    L.kernel = p.kernel;
+    const bool partial = part_end >= 0;
+    if (!partial) {
+        part_begin = 0;
+        part_end = p.n_partitions();
+        L.row_begin = 0;
+        L.row_end = p.n_rows;
+    } else {
+        require(p.kernel == PSC_KERNEL_SPMV, "bind_partitions: only SpMV plans shard by partition");
+        require(0 <= part_begin && part_begin <= part_end && part_end <= p.n_partitions(),
+                "bind_partitions: partition range out of bounds");
+        int64_t g0 = p.part_group_ptr[part_begin], g1 = p.part_group_ptr[part_end];
+        int32_t rb = p.n_rows, re = 0;
+        int64_t rows = 0;
+        for (int64_t g = g0; g < g1; ++g) {
+            rb = std::min(rb, p.g_row_begin[g]);
+            re = std::max(re, p.g_row_end[g]);
+            rows += p.g_row_end[g] - p.g_row_begin[g];
+        }
+        if (g0 == g1) rb = re = 0;
+        require(rows == static_cast<int64_t>(re) - rb, "bind_partitions: partitions do not cover a contiguous row range");
+        L.row_begin = rb;
+        L.row_end = re;
+    }
+    L.k_begin = ro[L.row_begin];
+    L.k_end = ro[L.row_end];
+    const int32_t nr = L.row_end - L.row_begin;
+    const int64_t g0 = p.part_group_ptr[part_begin], g1 = p.part_group_ptr[part_end];
+    if (force_general) {
+        require(!partial, "bind_partitions: the general interpreter binds whole plans only");
+        L.canonical = false;
+        L.why_general = "execute_plan accumulates onto the caller's arrays";
+        build_general(p, a, L);
+        return L;
+    }
+
+    // ---- collect segments in plan order; decide canonicality ----
+    std::vector<int32_t> count(static_cast<std::size_t>(nr) + 1, 0);
+    std::vector<SegRec> segs;
+    auto non_canonical = [&](const std::string& why) {
+        if (L.canonical) L.why_general = why;
+        L.canonical = false;
+    };
+    std::vector<int64_t> fin_part;      // sptrsv: partition of each row's finalize
+    std::vector<int64_t> fin_group;
+    if (p.kernel == PSC_KERNEL_SPTRSV) {
+        fin_part.assign(p.n_rows, -1);
+        fin_group.assign(p.n_rows, -1);
+        for (int64_t part = part_begin; part < part_end && L.canonical; ++part) {
+            for (int64_t g = p.part_group_ptr[part]; g < p.part_group_ptr[part + 1]; ++g) {
+                auto visit = [&](int32_t r, int32_t dpos, int32_t rhs) {
+                    if (r < 0 || r >= p.n_rows || dpos != ro[r + 1] - 1 || rhs != r || fin_part[r] >= 0) {
+                        non_canonical("finalize records are not one {r, diag(r), r} per row");
+                        return;
+                    }
+                    fin_part[r] = part;
+                    fin_group[r] = g;
+                };
+                if (p.mined) {
+                    for (int32_t r = p.g_row_begin[g]; r < p.g_row_end[g]; ++r) visit(r, ro[r + 1] - 1, r);
+                } else {
+                    for (int64_t f = p.g_fin_ptr[g]; f < p.g_fin_ptr[g + 1]; ++f) visit(p.f_row[f], p.f_diag[f], p.f_rhs[f]);
+                }
+            }
+        }
+        for (int32_t r = 0; r < p.n_rows && L.canonical; ++r)
+            if (fin_part[r] < 0) non_canonical("a row has no finalize record");
+    }
+    segs.reserve(static_cast<std::size_t>(p.g_codelet_ptr[g1] - p.g_codelet_ptr[g0]));
+    for (int64_t part = part_begin; part < part_end && L.canonical; ++part) {
+        for (int64_t g = p.part_group_ptr[part]; g < p.part_group_ptr[part + 1] && L.canonical; ++g) {
+            for (int64_t c = p.g_codelet_ptr[g]; c < p.g_codelet_ptr[g + 1] && L.canonical; ++c) {
+                const int m = p.c_m[c], n = p.c_n[c];
+                if (p.mined) {
+                    const bool blas = p.c_kind[c] == PSC_CODELET_BLAS;
+                    for (int i = 0; i < m; ++i) {
+                        int32_t r = p.c_row[c] + i;
+                        int64_t s = static_cast<int64_t>(p.c_mat_base[c]) + static_cast<int64_t>(i) * p.c_mat_so[c];
+                        segs.push_back({r - L.row_begin, static_cast<int32_t>(s - L.k_begin), n,
+                                        blas ? p.c_vec_base[c] + i * p.c_vec_so[c] : -1});
+                        ++count[r - L.row_begin];
+                    }
+                    continue;
+                }
+                // imported codelet: check every canonical invariant
+                const int which = dispatch_kind(p.c_kind[c]);
+                DescView ds[3] = {p.desc(c, 0), p.desc(c, 1), p.desc(c, 2)};
+                check_codelet_shape(which, ds[0].form, ds[1].form, ds[2].form);
+                if (m <= 0 || n <= 0) continue;
+                if (n > 1 && ds[1].si != 1) {
+                    non_canonical("non-unit matrix inner stride");
+                    break;
+                }
+                if (p.kernel == PSC_KERNEL_SPMV && which == PSC_CODELET_BLAS && n >= 4 && ds[2].si != 1) {
+                    non_canonical("BLAS gather with non-unit inner stride takes the sequential branch");
+                    break;
+                }
+                for (int i = 0; i < m && L.canonical; ++i) {
+                    int64_t o = which == PSC_CODELET_PSC_II ? tab_at(p, ds[0], c, 0, i, a)
+                                                            : static_cast<int64_t>(ds[0].base) + static_cast<int64_t>(i) * ds[0].so;
+                    if (o < L.row_begin || o >= L.row_end) {
+                        non_canonical("output index outside the bound rows");
+                        break;
+                    }
+                    int64_t s = static_cast<int64_t>(ds[1].base) + static_cast<int64_t>(i) * ds[1].so;
+                    if (s < ro[o] || s + n > static_cast<int64_t>(ro[o + 1]) - sp) {
+                        non_canonical("codelet row does not lie in its output row");
+                        break;
+                    }
+                    bool unit_run = which == PSC_CODELET_BLAS && (ds[2].si == 1 || n == 1);
+                    int64_t v0 = 0;
+                    for (int j = 0; j < n; ++j) {
+                        int64_t xv;
+                        if (which == PSC_CODELET_BLAS) {
+                            xv = static_cast<int64_t>(ds[2].base) + static_cast<int64_t>(i) * ds[2].so +
+                                 static_cast<int64_t>(j) * ds[2].si;
+                        } else {
+                            bool per_point = which == PSC_CODELET_PSC_II && ds[2].form == PSC_FORM_POINT_TABLE;
+                            xv = tab_at(p, ds[2], c, 2, per_point ? static_cast<int64_t>(i) * n + j : j, a);
+                        }
+                        if (j == 0) v0 = xv;
+                        if (xv != a.col_indices[s + j]) {
+                            non_canonical("gather differs from col_indices");
+                            break;
+                        }
+                    }
+                    if (!L.canonical) break;
+                    if (p.kernel == PSC_KERNEL_SPTRSV) {
+                        // must run before its row's finalize, in the same group
+                        // when in the same partition, after every x it reads
+                        if (fin_part[o] < part || (fin_part[o] == part && fin_group[o] != g)) {
+                            non_canonical("codelet of a row runs outside its finalize group");
+                            break;
+                        }
+                        for (int j = 0; j < n; ++j) {
+                            if (fin_part[a.col_indices[s + j]] >= part) {
+                                non_canonical("codelet reads x before it is finalised");
+                                break;
+                            }
+                        }
+                        if (!L.canonical) break;
+                    }
+                    segs.push_back({static_cast<int32_t>(o - L.row_begin), static_cast<int32_t>(s - L.k_begin), n,
+                                    unit_run ? static_cast<int32_t>(v0) : -1});
+                    ++count[o - L.row_begin];
+                }
+            }
+        }
+    }
+    if (p.kernel == PSC_KERNEL_SPTRSV && p.mined && L.canonical) {
+        // level sets guarantee finalize-before-read; nothing to check
+    }
+
+    if (!L.canonical) {
+        require(!partial, "bind_partitions: plan is not canonical (" + L.why_general + ")");
+        segs.clear();
+        segs.shrink_to_fit();
+        build_general(p, a, L);
+        return L;
+    }
+
+    // ---- per-row segment lists (stable by plan order) ----
+    L.row_seg_ptr.assign(static_cast<std::size_t>(nr) + 1, 0);
+    for (int32_t r = 0; r < nr; ++r) L.row_seg_ptr[r + 1] = L.row_seg_ptr[r] + count[r];
+    const int64_t S = static_cast<int64_t>(segs.size());
+    require(S <= INT32_MAX, "bind: too many segments");
+    L.seg_start.resize(S);
+    L.seg_len.resize(S);
+    L.seg_vec.resize(S);
+    {
+        std::vector<int32_t> cur(L.row_seg_ptr.begin(), L.row_seg_ptr.end() - 1);
+        for (const SegRec& s : segs) {
+            int32_t k = cur[s.row]++;
+            L.seg_start[k] = s.start;
+            L.seg_len[k] = s.len;
+            L.seg_vec[k] = s.vec;
+        }
+    }
+    segs.clear();
+    segs.shrink_to_fit();
+    L.simple = true;
+    for (int32_t r = 0; r < nr && L.simple; ++r) {
+        int32_t gr = r + L.row_begin;
+        int32_t ext = ro[gr + 1] - ro[gr] - sp;
+        int32_t c = L.row_seg_ptr[r + 1] - L.row_seg_ptr[r];
+        if (c == 0) {
+            L.simple = ext == 0;
+        } else if (c == 1) {
+            int32_t k = L.row_seg_ptr[r];
+            L.simple = L.seg_start[k] == ro[gr] - L.k_begin && L.seg_len[k] == ext;
+        } else {
+            L.simple = false;
+        }
+    }
+    if (L.simple) {
+        L.row_seg_ptr.clear();
+        L.seg_start.clear();
+        L.seg_len.clear();
+        L.seg_vec.clear();
+        L.row_seg_ptr.shrink_to_fit();
+        L.seg_start.shrink_to_fit();
+        L.seg_len.shrink_to_fit();
+        L.seg_vec.shrink_to_fit();
+    }
+
+    // ---- work units ----
+    if (p.kernel == PSC_KERNEL_SPMV) {
+        L.chunk_row.push_back(0);
+        int64_t acc = 0;
+        for (int32_t r = 0; r < nr; ++r) {
+            int64_t len = ro[r + L.row_begin + 1] - ro[r + L.row_begin];
+            if (len > kSpmvChunk) {
+                if (L.chunk_row.back() != r) L.chunk_row.push_back(r);
+                L.chunk_row.push_back(r + 1);
+                ++L.long_rows;
+                acc = 0;
+                continue;
+            }
+            if (acc + len > kSpmvChunk) {
+                L.chunk_row.push_back(r);
+                acc = 0;
+            }
+            acc += len;
+        }
+        if (L.chunk_row.back() != nr) L.chunk_row.push_back(nr);
+    } else {
+        int R = sptrsv_block_rows;
+        if (R <= 0) {
+            if (const char* env = std::getenv("PSC_SPTRSV_BLOCK_ROWS")) R = std::atoi(env);
+        }
+        if (R <= 0) R = std::max(1024, (nr + 147) / 148);
+        R = std::min(R, 24576);
+        R = std::max(1, std::min(R, std::max(1, nr)));
+        L.block_row.push_back(0);
+        for (int32_t r = 0; r < nr;) {
+            int32_t e = static_cast<int32_t>(std::min<int64_t>(nr, static_cast<int64_t>(r) + R));
+            L.block_row.push_back(e);
+            L.max_block_rows = std::max(L.max_block_rows, e - r);
+            r = e;
+        }
+    }
+    return L;
+}
+
+Lowered lower_single_codelet(const psc_codelet_view& cv, int which) {
+    check_codelet_shape(which, cv.out.form, cv.mat.form, cv.vec.form);
+    Plan p;
+    p.mined = false;
+    p.kernel = PSC_KERNEL_SPMV;
+    p.part_group_ptr = {0, 1};
+    p.g_row_begin = {0};
+    p.g_row_end = {0};
+    p.g_strategy = {0};
+    p.g_cost = {0};
+    p.g_codelet_ptr = {0, 1};
+    p.g_fin_ptr = {0, 0};
+    p.c_kind = {static_cast<uint8_t>(which)};
+    p.c_m = {cv.outer_extent};
+    p.c_n = {cv.inner_extent};
+    const psc_access_desc_view* ds[3] = {&cv.out, &cv.mat, &cv.vec};
+    p.d_tab_ptr = {0};
+    for (int d = 0; d < 3; ++d) {
+        p.d_form.push_back(ds[d]->form);
+        p.d_base.push_back(ds[d]->base);
+        p.d_so.push_back(ds[d]->stride_outer);
+        p.d_si.push_back(ds[d]->stride_inner);
+        if (ds[d]->form != PSC_FORM_STRIDED && ds[d]->table_len > 0) {
+            require(ds[d]->table != nullptr, "codelet: null table");
+            p.tables.insert(p.tables.end(), ds[d]->table, ds[d]->table + ds[d]->table_len);
+        }
+        p.d_tab_ptr.push_back(static_cast<int64_t>(p.tables.size()));
+    }
+    Lowered L;
+    L.canonical = false;
+    L.why_general = "single codelet";
+    psc_csr_view none{0, 0, INT32_MAX, nullptr, nullptr, nullptr};
+    none.n_rows = INT32_MAX;
+    none.n_cols = INT32_MAX;
+    build_general(p, none, L);
+    return L;
+}
+
+}  // namespace pscb

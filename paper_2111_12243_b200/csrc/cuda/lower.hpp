@@ -1,0 +1,74 @@
+// Lowering of a codelet plan to the device layout (host side).
+//
+// Canonical plans (every plan the reference miner emits, and any imported
+// plan with the same invariants) become per-row *segments*: codelet row i of
+// codelet c contributes the contiguous CSR range [mat.base + i*mat.so, +n) to
+// output row out(i), and its gather equals col_indices over that range
+// (validate_plan enforces the gather identity, miner.cpp:346-366). A row's
+// result is the sum of its segment partials in plan order, each partial
+// formed exactly as exec_*_codelet forms it (4-lane dot for SpMV, sequential
+// for the solve; executor.cpp:23-116). When every row is a single segment
+// covering its whole operation range, no segment arrays are stored.
+//
+// Anything else (hand-built codelets with arbitrary tables, non-unit inner
+// strides, rows split across groups, solve plans that read x before it is
+// finalised) lowers to the general interpreter: one launch per partition, one
+// thread per region group, exact Listing-3 semantics.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+#include "psc_b200.h"
+
+namespace pscb {
+
+struct Lowered {
+    int kernel = PSC_KERNEL_SPMV;
+    int32_t row_begin = 0, row_end = 0;  // bound rows [row_begin, row_end)
+    int64_t k_begin = 0, k_end = 0;      // CSR positions of those rows
+    bool canonical = true;
+    bool simple = true;  // every row = one implicit full-row segment
+    // segments (local rows), only when canonical && !simple
+    std::vector<int32_t> row_seg_ptr;
+    std::vector<int32_t> seg_start;  // local CSR position
+    std::vector<int32_t> seg_len;
+    std::vector<int32_t> seg_vec;  // x index of element 0 when the gather is a unit-stride run, else -1
+    // SpMV work units: chunk boundaries in local rows
+    std::vector<int32_t> chunk_row;
+    int64_t long_rows = 0;
+    // SpTRSV row blocks in local rows
+    std::vector<int32_t> block_row;
+    int32_t max_block_rows = 0;
+    std::string why_general;  // reason the plan is not canonical
+
+    // general interpreter tables (only when !canonical)
+    struct General {
+        std::vector<int64_t> part_group_ptr;
+        std::vector<int64_t> group_codelet_ptr, group_fin_ptr;
+        std::vector<int32_t> c_kind, c_m, c_n;
+        std::vector<int32_t> d_form, d_base, d_so, d_si;  // 3 per codelet
+        std::vector<int64_t> d_tab;                       // 3 per codelet: offset into tables
+        std::vector<int32_t> tables;
+        std::vector<int32_t> f_row, f_diag, f_rhs;
+        int64_t max_mat = -1, max_vec = -1, max_out = -1;  // touched index ranges
+    } gen;
+};
+
+constexpr int kSpmvChunk = 2048;  // products staged in shared memory per CTA
+
+// Lower partitions [part_begin, part_end) (all partitions when part_end < 0).
+// force_general lowers through the exact interpreter even when canonical
+// (execute_plan accumulates onto caller-provided accum/solution arrays).
+Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int64_t part_end,
+                   int sptrsv_block_rows, bool force_general = false);
+
+// Build a general-path lowering of one hand-built codelet (exec_*_codelet).
+Lowered lower_single_codelet(const psc_codelet_view& c, int which);
+
+// Shape checks of exec_*_codelet (executor.cpp:54-56, 76-78, 97-99).
+void check_codelet_shape(int which, int out_form, int mat_form, int vec_form);
+
+}  // namespace pscb

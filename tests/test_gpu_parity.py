@@ -1,0 +1,153 @@
+"""GPU parity: the sm_100a executor against the C oracle (oracle/psc_oracle.c,
+itself pinned bitwise to the reference executor in test_oracle.py).
+
+Bar: bitwise equality with the reference executor's arithmetic (parity mode)
+on every plan, exact equality with the naive baseline on integer data
+(acceptance_main.cpp:156-157), and the reference's 1e-12 elementwise bound on
+the random suite."""
+import numpy as np
+import pytest
+
+import paper_2111_12243_b200 as P
+from oracle.oracle import Oracle
+from paper_2111_12243_b200 import KernelKind
+from tests.helpers import bitwise_equal, max_rel_err, normwise_err, suite_cases, suite_input
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(exe, plan, kernel, a, vec):
+    if kernel == KernelKind.Spmv:
+        y = np.full(a.n_rows, np.nan)
+        P.run_spmv(plan, a, vec, y, exe)
+        return y
+    x = np.full(a.n_rows, np.nan)
+    acc = np.full(a.n_rows, np.nan)
+    P.run_sptrsv(plan, P.TriangularMatrix.adopt(a), vec, x, acc, exe)
+    return x
+
+
+def run_oracle(plan, kernel, a, vec):
+    if kernel == KernelKind.Spmv:
+        return Oracle.run_spmv(plan.export_arrays(), a.view(), vec)
+    return Oracle.run_sptrsv(plan.export_arrays(), a.view(), vec)[0]
+
+
+def baseline(kernel, a, vec):
+    if kernel == KernelKind.Spmv:
+        return Oracle.spmv_baseline(a.view(), vec)
+    return Oracle.sptrsv_baseline(a.view(), vec)
+
+
+def test_acceptance_suite_bitwise(exe):
+    """acceptance_main.cpp:127-174: 42 cases x t in {1,2,3,8} x groups in {1,4} = 336 plans."""
+    n_plans = mismatches = 0
+    for name, kernel, a, ints in suite_cases():
+        vec = suite_input(kernel, a, ints)
+        want = baseline(kernel, a, vec)
+        for t in (1, 2, 3, 8):
+            for groups in (1, 4):
+                plan = P.inspect(kernel, a, t, groups)
+                got = run_gpu(exe, plan, kernel, a, vec)
+                ref = run_oracle(plan, kernel, a, vec)
+                assert bitwise_equal(got, ref), f"{name} t={t} groups={groups}: not bitwise equal to the executor"
+                ok = bitwise_equal(got, want) if ints else max_rel_err(got, want) <= 1e-12
+                mismatches += 0 if ok else 1
+                n_plans += 1
+    assert n_plans == 336 and mismatches == 0
+
+
+@pytest.mark.parametrize("config,scale,kernel", [
+    (1, 1.0, KernelKind.Spmv),
+    (2, 1.0, KernelKind.Sptrsv),
+    (3, 0.05, KernelKind.Spmv),
+    (4, 0.1, KernelKind.Sptrsv),
+    (5, 0.02, KernelKind.Spmv),
+])
+def test_configs_bitwise(exe, config, scale, kernel):
+    a = P.generate_config(config, scale)
+    plan = P.inspect(kernel, a, 3, 8)
+    vec = P.uniform_vector(a.n_cols, 10 + config)
+    got = run_gpu(exe, plan, kernel, a, vec)
+    assert bitwise_equal(got, run_oracle(plan, kernel, a, vec))
+    tol = 1e-12 if kernel == KernelKind.Spmv else 1e-10
+    assert normwise_err(got, baseline(kernel, a, vec)) <= tol
+
+
+def test_bound_device_path_matches_host_path(exe):
+    import torch
+
+    a = P.generate_config(2, 0.02)
+    plan = P.inspect(KernelKind.Sptrsv, a, 3, 8)
+    b = P.uniform_vector(a.n_rows, 3)
+    host = run_gpu(exe, plan, KernelKind.Sptrsv, a, b)
+    bound = P.BoundPlan(exe, plan, a)
+    bd = torch.from_numpy(b).cuda()
+    xd = torch.empty_like(bd)
+    accd = torch.empty_like(bd)
+    for _ in range(3):  # repeated solves re-arm correctly
+        bound.sptrsv(bd, xd, accd)
+    torch.cuda.synchronize()
+    assert bitwise_equal(xd.cpu().numpy(), host)
+    xh = np.empty_like(b)
+    bound.sptrsv_host(b, xh)
+    torch.cuda.synchronize()
+    assert bitwise_equal(xh, host)
+
+
+# ---- exec_*_codelet known answers (test_executor.cpp:37-114) ----
+
+def _ctx(ax, x, acc, rhs=None):
+    return P.ExecutionContext(np.array(ax, float), np.array(x, float), acc, rhs)
+
+
+def test_blas_codelet_known_answers():
+    c = P.Codelet(P.CodeletKind.Blas, 3, 3, P.AccessDesc.strided(0, 1, 0), P.AccessDesc.strided(0, 3, 1),
+                  P.AccessDesc.strided(0, 0, 1))
+    acc = np.zeros(3)
+    P.exec_blas_codelet(c, _ctx(range(1, 10), [1, 1, 1], acc))
+    assert acc.tolist() == [6, 15, 24]
+    c.vec = P.AccessDesc.strided(0, 0, 2)  # non-unit inner stride: sequential branch
+    acc = np.zeros(3)
+    P.exec_blas_codelet(c, _ctx(range(1, 10), [1, 0, 1, 0, 1, 0], acc))
+    assert acc.tolist() == [6, 15, 24]
+    one = P.Codelet(P.CodeletKind.Blas, 1, 1, P.AccessDesc.strided(2, 0, 0), P.AccessDesc.strided(1, 0, 1),
+                    P.AccessDesc.strided(3, 0, 1))
+    acc = np.ones(3)
+    P.exec_blas_codelet(one, _ctx([0, 5, 0], [0, 0, 0, 4], acc))
+    assert acc.tolist() == [1, 1, 21]
+
+
+def test_psc_codelet_known_answers():
+    c = P.Codelet(P.CodeletKind.PscI, 3, 3, P.AccessDesc.strided(0, 1, 0), P.AccessDesc.strided(0, 3, 1),
+                  P.AccessDesc.inner_table([0, 2, 5]))
+    acc = np.zeros(3)
+    P.exec_psci_codelet(c, _ctx(range(1, 10), [10, 0, 20, 0, 0, 30], acc))
+    assert acc.tolist() == [140, 320, 500]
+    c2 = P.Codelet(P.CodeletKind.PscII, 1, 2, P.AccessDesc.outer_table([0]), P.AccessDesc.strided(0, 0, 1),
+                   P.AccessDesc.inner_table([1, 3]))
+    acc = np.zeros(1)
+    P.exec_pscii_codelet(c2, _ctx([2, 5], [0, 1, 0, 1], acc))
+    assert acc.tolist() == [7]
+    f = P.Codelet(P.CodeletKind.PscII, 2, 1, P.AccessDesc.outer_table([0, 1]), P.AccessDesc.strided(0, 1, 1),
+                  P.AccessDesc.point_table([1, 3]))
+    acc = np.zeros(2)
+    P.exec_pscii_codelet(f, _ctx([2, 5], [0, 1, 0, 1], acc))
+    assert acc.tolist() == [2, 5]
+
+
+def test_codelet_shape_errors():
+    """test_executor.cpp:116-138."""
+    c = P.Codelet(P.CodeletKind.Blas, 1, 1, P.AccessDesc.strided(0, 0, 0), P.AccessDesc.strided(0, 0, 1),
+                  P.AccessDesc.inner_table([0]))
+    ctx = _ctx([1], [1], np.zeros(1))
+    with pytest.raises(P.InvalidArgument):
+        P.exec_blas_codelet(c, ctx)
+    c.vec = P.AccessDesc.strided(0, 0, 1)
+    with pytest.raises(P.InvalidArgument):
+        P.exec_psci_codelet(c, ctx)
+    with pytest.raises(P.InvalidArgument):
+        P.exec_pscii_codelet(c, ctx)
+    c.out, c.mat, c.vec = P.AccessDesc.outer_table([0]), P.AccessDesc.inner_table([0]), P.AccessDesc.inner_table([0])
+    with pytest.raises(P.InvalidArgument):
+        P.exec_pscii_codelet(c, ctx)
