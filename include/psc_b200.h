@@ -188,6 +188,10 @@ PSC_API psc_status psc_bound_sptrsv(psc_bound* b, const double* b_dev, double* x
 PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x_host, double* y_host, void* stream);
 PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* b_host, double* x_host,
                                          double* acc_host /* nullable */, void* stream);
+/* Diagnostics (PSC_TRSV_TRACE=1 at bind): per-row publish times of the last
+ * solve in ns (%globaltimer), then one arm time per row block. Returns the
+ * number of entries copied (0 when tracing is off). */
+PSC_API int64_t psc_bound_trace(const psc_bound* b, uint64_t* out, int64_t cap);
 /* Number of kernel launches one psc_bound_* call enqueues. */
 PSC_API int32_t psc_bound_launches(const psc_bound* b);
 /* Lowering diagnostics, out[0..7]: rows, segments (0 = every row is one

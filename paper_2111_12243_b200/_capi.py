@@ -133,6 +133,7 @@ _SIGS = {
     "psc_bound_sptrsv": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "psc_bound_spmv_host": (c_int32, [c_void_p, POINTER(c_double), POINTER(c_double), c_void_p]),
     "psc_bound_sptrsv_host": (c_int32, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_double), c_void_p]),
+    "psc_bound_trace": (c_int64, [c_void_p, POINTER(c_uint64), c_int64]),
     "psc_bound_launches": (c_int32, [c_void_p]),
     "psc_bound_info": (c_int32, [c_void_p, POINTER(c_int64)]),
     "psc_run_spmv": (

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -75,7 +76,14 @@ struct psc_bound {
     std::string why_general;
     DevBuf ro, col, val;
     DevBuf rsp, sst, slen, svec, chunk_row, ticket, armed;
+    bool chain_mode = false;
+    int max_block_units = 0;
+    DevBuf block_row, block_unit, unit_start;
     int32_t epoch = 0;      // per-launch arming epoch of the solve kernel
+    DevBuf trace;           // PSC_TRSV_TRACE=1: per-row publish times (diagnostics)
+    int trsv_threads = 256; // CTA size of the solve kernel (PSC_TRSV_THREADS)
+    int trsv_lat = 700;     // cycles before a lane inspects a load it issued (PSC_TRSV_LAT)
+    bool trsv_lean = false; // lean round kernel: simple rows with <= 4 off-diagonal entries
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
     // general path
     std::vector<int64_t> part_group_ptr;
@@ -101,7 +109,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &ticket, &armed, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &ticket, &armed, &block_row, &block_unit, &unit_start, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -174,9 +182,39 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->long_rows = L.long_rows;
         } else {
             b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
+            b->chain_mode = L.chain_mode;
+            b->block_row.upload(L.block_row, s);
+            b->block_unit.upload(L.block_unit, s);
+            b->unit_start.upload(L.unit_start, s);
+            b->max_block_units = L.max_block_units;
+            // CTA size: enough lanes for the units of a block (chain mode) or
+            // 256 (row mode), within the shared-memory budget
+            int th = 256;
+            if (L.chain_mode) {
+                th = 64;
+                while (th < 512 && th < L.max_block_units) th *= 2;
+            }
+            if (const char* env = std::getenv("PSC_TRSV_THREADS")) th = std::atoi(env);
+            auto smem_of = [&](int t) { return sptrsv_smem_bytes(t, L.max_block_rows, L.max_block_units); };
+            while (th > 64 && smem_of(th) > 232448) th /= 2;
+            require(smem_of(th) <= 232448, "bind: solve block does not fit in shared memory");
+            b->trsv_threads = th;
             b->max_block_rows = L.max_block_rows;
             b->ticket.ensure(2 * sizeof(int32_t));
             ck(cudaMemsetAsync(b->ticket.p, 0, 2 * sizeof(int32_t), s), "memset");
+            if (const char* tr = std::getenv("PSC_TRSV_TRACE"); tr && tr[0] == '1') {
+                const size_t nt = static_cast<size_t>(b->rows()) + b->n_blocks + 1;
+                b->trace.ensure(nt * sizeof(unsigned long long));
+                ck(cudaMemsetAsync(b->trace.p, 0, nt * sizeof(unsigned long long), s), "memset");
+            }
+            if (const char* tl = std::getenv("PSC_TRSV_LAT")) b->trsv_lat = std::atoi(tl);
+            {
+                int32_t max_ext = 0;
+                for (int32_t r = L.row_begin; r < L.row_end; ++r)
+                    max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
+                b->trsv_lean = L.simple && max_ext <= 4;
+                if (const char* ln = std::getenv("PSC_TRSV_LEAN")) b->trsv_lean = b->trsv_lean && ln[0] == '1';
+            }
             b->armed.ensure(std::max(1, b->n_blocks) * sizeof(int32_t));
             ck(cudaMemsetAsync(b->armed.p, 0, std::max(1, b->n_blocks) * sizeof(int32_t), s), "memset");
         }
@@ -230,9 +268,11 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
     use_device(b->device);
     if (b->canonical) {
         b->epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;
-        launch_sptrsv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc, b->rows(),
-                             b->max_block_rows, b->segs(), b->ticket.as<int32_t>(), b->armed.as<int32_t>(), b->epoch,
-                             s);
+        launch_sptrsv(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,
+                      b->block_row.as<int32_t>(), b->block_unit.as<int32_t>(), b->unit_start.as<int32_t>(), b->n_blocks,
+                      b->max_block_rows, b->max_block_units, !b->chain_mode, b->segs(), b->ticket.as<int32_t>(),
+                      b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
+                      b->trsv_lean ? -b->trsv_lat : b->trsv_lat, s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");
@@ -364,6 +404,17 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
         ck(cudaMemcpyAsync(x, b->hx.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
         if (acc) ck(cudaMemcpyAsync(acc, b->hacc.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
     });
+}
+// Diagnostics: copies the per-row publish times of the last solve (ns,
+// %globaltimer) followed by one arm time per block; needs PSC_TRSV_TRACE=1
+// at bind time. Returns the number of entries copied.
+PSC_API int64_t psc_bound_trace(const psc_bound* b, uint64_t* out, int64_t cap) {
+    if (!b || !b->trace.p || !out) return 0;
+    int64_t n = std::min<int64_t>(cap, static_cast<int64_t>(b->trace.bytes / sizeof(uint64_t)));
+    if (cudaSetDevice(b->device) != cudaSuccess) return 0;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+    if (cudaMemcpy(out, b->trace.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+    return n;
 }
 PSC_API int32_t psc_bound_launches(const psc_bound* b) {
     if (!b) return 0;

@@ -23,12 +23,19 @@ void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val
                         double* y, const int32_t* chunk_row, int n_chunks, SegmentsDev segs,
                         bool accumulate, cudaStream_t stream);
 
-// Sync-free blocked triangular solve over uniform row blocks of block_rows
-// rows. ticket: 2 zeroed ints, left zeroed on exit; armed: one int per block,
-// epoch must differ from every value armed[] holds (a per-launch counter).
-void launch_sptrsv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* b,
-                          double* x, double* acc_out, int n_rows, int block_rows, SegmentsDev segs,
-                          int32_t* ticket, int32_t* armed, int epoch, cudaStream_t stream);
+// Sync-free blocked triangular solve (kernels.cu, "blocked sync-free
+// triangular solve"): blocks [block_row[i], block_row[i+1]) of rows, solved by
+// units listed in unit_start[block_unit[i] .. block_unit[i+1]) -- runs of
+// consecutive rows (chain mode) or single rows in level order
+// (single_row_units). ticket: 2 zeroed ints, left zeroed; armed: one int per
+// block, epoch a per-launch counter. trace (nullable) gets per-row publish
+// times followed by one arm time per block.
+void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, const double* b, double* x,
+                   double* acc_out, const int32_t* block_row, const int32_t* block_unit, const int32_t* unit_start,
+                   int n_blocks, int max_rows, int max_units, bool single_row_units, SegmentsDev segs,
+                   int32_t* ticket, int32_t* armed, int epoch, unsigned long long* trace, int threads,
+                   int poll_latency, cudaStream_t stream);
+size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units);
 
 // General interpreter (exact Listing-3 semantics) over groups [g0, g1) of one
 // partition; one thread per region group.

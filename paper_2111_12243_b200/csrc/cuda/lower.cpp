@@ -357,19 +357,63 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
         }
         if (L.chunk_row.back() != nr) L.chunk_row.push_back(nr);
     } else {
+        // Units: a row continues the unit of the row above when it reads it
+        // (its last off-diagonal entry is column r-1).
+        std::vector<uint8_t> cont(nr, 0);
+        int64_t n_units = 0;
+        for (int32_t r = 0; r < nr; ++r) {
+            const int32_t gr = r + L.row_begin;
+            const int32_t k0 = ro[gr], kd = ro[gr + 1] - 1;
+            cont[r] = r > 0 && kd > k0 && a.col_indices[kd - 1] == gr - 1;
+            n_units += !cont[r];
+        }
+        const double avg_unit = n_units ? static_cast<double>(nr) / static_cast<double>(n_units) : 0.0;
+        int mode = -1;  // PSC_TRSV_MODE: 0 rows, 1 chains; default by average unit length
+        if (const char* env = std::getenv("PSC_TRSV_MODE")) mode = std::atoi(env);
+        L.chain_mode = mode == 1 || (mode != 0 && avg_unit >= 4.0);
         int R = sptrsv_block_rows;
         if (R <= 0) {
             if (const char* env = std::getenv("PSC_SPTRSV_BLOCK_ROWS")) R = std::atoi(env);
         }
-        if (R <= 0) R = std::max(1024, (nr + 147) / 148);
-        R = std::min(R, 24576);
-        R = std::max(1, std::min(R, std::max(1, nr)));
         L.block_row.push_back(0);
-        for (int32_t r = 0; r < nr;) {
-            int32_t e = static_cast<int32_t>(std::min<int64_t>(nr, static_cast<int64_t>(r) + R));
-            L.block_row.push_back(e);
-            L.max_block_rows = std::max(L.max_block_rows, e - r);
-            r = e;
+        {
+            const int cap = L.chain_mode ? 12000 : 9000;  // shared-memory rows per CTA (kernels.cu smem layout)
+            if (R <= 0) R = std::max(1024, (nr + 99) / 100);  // ~100 blocks
+            R = std::max(1, std::min({R, cap, std::max(1, nr)}));
+            for (int32_t r = 0; r < nr;) {
+                int32_t e = static_cast<int32_t>(std::min<int64_t>(nr, static_cast<int64_t>(r) + R));
+                L.block_row.push_back(e);
+                L.max_block_rows = std::max(L.max_block_rows, e - r);
+                r = e;
+            }
+        }
+        if (L.chain_mode) {
+            L.block_unit.push_back(0);
+            for (size_t bi = 0; bi + 1 < L.block_row.size(); ++bi) {
+                const int32_t b0 = L.block_row[bi], b1 = L.block_row[bi + 1];
+                const int64_t u0 = static_cast<int64_t>(L.unit_start.size());
+                for (int32_t r = b0; r < b1; ++r)
+                    if (r == b0 || !cont[r]) L.unit_start.push_back(r);
+                L.block_unit.push_back(static_cast<int32_t>(L.unit_start.size()));
+                L.max_block_units = std::max<int32_t>(L.max_block_units, static_cast<int32_t>(L.unit_start.size() - u0));
+            }
+        } else {
+            // level of every row = partition of its finalize record; within a
+            // block, rows are listed by (level, row) so threads take them in a
+            // dependency-respecting order
+            std::vector<int32_t> lvl(nr, 0);
+            if (!fin_part.empty()) {
+                for (int32_t r = 0; r < nr; ++r) lvl[r] = static_cast<int32_t>(fin_part[r]);
+            }
+            L.unit_start.resize(nr);
+            for (size_t bi = 0; bi + 1 < L.block_row.size(); ++bi) {
+                int32_t b0 = L.block_row[bi], b1 = L.block_row[bi + 1];
+                for (int32_t r = b0; r < b1; ++r) L.unit_start[r] = r;
+                std::stable_sort(L.unit_start.begin() + b0, L.unit_start.begin() + b1,
+                                 [&](int32_t u, int32_t v) { return lvl[u] < lvl[v]; });
+            }
+            L.block_unit = L.block_row;  // one unit per row
+            L.max_block_units = L.max_block_rows;
         }
     }
     return L;

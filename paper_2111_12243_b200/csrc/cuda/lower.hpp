@@ -39,8 +39,15 @@ struct Lowered {
     // SpMV work units: chunk boundaries in local rows
     std::vector<int32_t> chunk_row;
     int64_t long_rows = 0;
-    // SpTRSV row blocks in local rows
+    // SpTRSV row blocks in local rows, and every block's rows in
+    // dependency-level order (the plan's partition index, then row)
     std::vector<int32_t> block_row;
+    // units solved front to back by one lane: chain mode -- runs of
+    // consecutive rows each reading the row above, listed in row order; row
+    // mode -- single rows listed by (level, row). block_unit = unit ranges.
+    bool chain_mode = false;
+    std::vector<int32_t> unit_start, block_unit;
+    int32_t max_block_units = 0;
     int32_t max_block_rows = 0;
     std::string why_general;  // reason the plan is not canonical
 
