@@ -149,6 +149,11 @@ PSC_API psc_status psc_plan_from_arrays(const psc_plan_counts* counts,
 PSC_API psc_status psc_plan_hash(const psc_plan* plan, const psc_csr_view* a, uint64_t* out);
 PSC_API psc_status psc_plan_totals(const psc_plan* plan, int64_t* total_cost, int64_t* total_ops,
                                    int64_t ops_by_kind[3]);
+/* Rows covered by partitions [part_begin, part_end): the union of their
+ * windows, which must be one contiguous range (SpMV balanced ranges,
+ * scheduler.cpp:67-89). Used to shard a plan over GPUs. */
+PSC_API psc_status psc_plan_partition_rows(const psc_plan* plan, int64_t part_begin, int64_t part_end,
+                                           int32_t* row_begin, int32_t* row_end);
 /* validate_plan (miner.cpp:325-395): PSC_ERR_LOGIC on violation. */
 PSC_API psc_status psc_validate_plan(const psc_plan* plan, const psc_csr_view* a);
 PSC_API void psc_plan_destroy(psc_plan* plan);

@@ -118,6 +118,7 @@ _SIGS = {
     "psc_plan_hash": (c_int32, [c_void_p, POINTER(CsrView), POINTER(c_uint64)]),
     "psc_plan_totals": (c_int32, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "psc_validate_plan": (c_int32, [c_void_p, POINTER(CsrView)]),
+    "psc_plan_partition_rows": (c_int32, [c_void_p, c_int64, c_int64, POINTER(c_int32), POINTER(c_int32)]),
     "psc_plan_destroy": (None, [c_void_p]),
     "psc_executor_create": (c_int32, [c_int32, c_int32, POINTER(c_void_p)]),
     "psc_executor_workers": (c_int32, [c_void_p]),

@@ -1,5 +1,6 @@
 // C ABI, host half: errors, matrices, generators, inspector and plans.
 // Executor / device entry points live in csrc/cuda/executor.cu.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -123,6 +124,28 @@ PSC_API psc_status psc_plan_totals(const psc_plan* plan, int64_t* total_cost, in
         if (total_cost) *total_cost = cost;
         if (total_ops) *total_ops = ops;
         if (ops_by_kind) std::memcpy(ops_by_kind, by, sizeof by);
+    });
+}
+PSC_API psc_status psc_plan_partition_rows(const psc_plan* plan, int64_t part_begin, int64_t part_end,
+                                           int32_t* row_begin, int32_t* row_end) {
+    return guarded([&] {
+        require(plan && row_begin && row_end, "psc_plan_partition_rows: null argument");
+        const Plan& p = plan->p;
+        require(0 <= part_begin && part_begin <= part_end && part_end <= p.n_partitions(),
+                "psc_plan_partition_rows: partition range out of bounds");
+        int64_t g0 = p.part_group_ptr[part_begin], g1 = p.part_group_ptr[part_end];
+        int32_t rb = p.n_rows, re = 0;
+        int64_t rows = 0;
+        for (int64_t g = g0; g < g1; ++g) {
+            rb = std::min(rb, p.g_row_begin[g]);
+            re = std::max(re, p.g_row_end[g]);
+            rows += p.g_row_end[g] - p.g_row_begin[g];
+        }
+        if (g0 == g1) rb = re = 0;
+        require(rows == static_cast<int64_t>(re) - rb,
+                "psc_plan_partition_rows: partitions do not cover a contiguous row range");
+        *row_begin = rb;
+        *row_end = re;
     });
 }
 PSC_API psc_status psc_validate_plan(const psc_plan* plan, const psc_csr_view* a) {

@@ -771,3 +771,10 @@ class BoundPlan:
 
 def device_count() -> int:
     return int(_capi.lib().psc_device_count())
+
+
+def partition_rows(plan: CodeletPlan, part_begin: int, part_end: int):
+    """Contiguous row range [begin, end) covered by partitions [part_begin, part_end)."""
+    rb, re = C.c_int32(), C.c_int32()
+    _check(_capi.lib().psc_plan_partition_rows(plan.handle, part_begin, part_end, C.byref(rb), C.byref(re)))
+    return rb.value, re.value

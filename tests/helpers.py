@@ -67,3 +67,34 @@ def normwise_err(got, want) -> float:
     den = float(np.max(np.abs(want))) if want.size else 0.0
     num = float(np.max(np.abs(np.asarray(got) - want))) if want.size else 0.0
     return num / den if den > 0 else num
+
+
+# ---- golden fixtures (tests/golden/make_golden.py, generated from the reference) ----
+import json as _json  # noqa: E402
+import os as _os  # noqa: E402
+
+_GOLDEN = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "golden")
+
+
+def golden_cases():
+    """[(meta, matrix, input vector, reference executor output, reference baseline output)]"""
+    with open(_os.path.join(_GOLDEN, "ref_golden.json")) as f:
+        index = _json.load(f)
+    data = np.load(_os.path.join(_GOLDEN, "ref_golden.npz"))
+    out = []
+    for i, meta in enumerate(index):
+        src = meta["src"]
+        if src[0] == "pattern":
+            a = P.generate_pattern(src[1])
+        elif src[0] == "pattern_unit_lower":
+            a = unit_lower(P.generate_pattern(src[1]))
+        else:
+            a = P.generate_config(int(src[1]), float(src[2]))
+        if meta["input"] == "int":
+            vec = P.int_vector(a.n_cols, 7)
+        elif meta["input"] == "seeded":
+            vec = P.seeded_vector(a.n_cols, 42)
+        else:
+            vec = P.uniform_vector(a.n_cols, 13, -1.0, 1.0)
+        out.append((meta, a, vec, data[f"c{i}_out"], data[f"c{i}_base"]))
+    return out

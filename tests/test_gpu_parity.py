@@ -151,3 +151,48 @@ def test_codelet_shape_errors():
     c.out, c.mat, c.vec = P.AccessDesc.outer_table([0]), P.AccessDesc.inner_table([0]), P.AccessDesc.inner_table([0])
     with pytest.raises(P.InvalidArgument):
         P.exec_pscii_codelet(c, ctx)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_partition_shards_bitwise(exe, world):
+    """Row shards bound by partition (multi-GPU path) equal the full plan's rows."""
+    import torch
+
+    from paper_2111_12243_b200.dist import shard_partitions
+
+    a = P.generate_config(5, 0.01)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(a.n_cols, 15)
+    want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+    xd = torch.from_numpy(x).cuda()
+    n_parts = plan.counts().n_partitions
+    for r in range(world):
+        p0, p1 = shard_partitions(n_parts, world, r)
+        if p1 == p0:
+            continue
+        bound = P.BoundPlan(exe, plan, a, partitions=(p0, p1))
+        y = torch.empty(bound.row_end - bound.row_begin, dtype=torch.float64, device="cuda")
+        bound.spmv(xd, y)
+        torch.cuda.synchronize()
+        assert bitwise_equal(y.cpu().numpy(), want[bound.row_begin:bound.row_end])
+
+
+def test_general_path_hand_built_plan(exe):
+    """A hand-built plan that is not canonical (shared out table, strided gather)
+    runs through the exact interpreter and matches the oracle bitwise."""
+    a = P.dense_block(4)
+    # rows 0 and 1 of the matrix accumulate into outputs 1 and 0 (crossed): not canonical
+    c1 = P.Codelet(P.CodeletKind.Blas, 2, 4, P.AccessDesc.strided(1, -1, 0), P.AccessDesc.strided(0, 4, 1),
+                   P.AccessDesc.strided(0, 0, 1))
+    c2 = P.Codelet(P.CodeletKind.PscII, 2, 4, P.AccessDesc.outer_table([2, 3]), P.AccessDesc.strided(8, 4, 1),
+                   P.AccessDesc.point_table([0, 1, 2, 3, 0, 1, 2, 3]))
+    g = P.RegionGroup(P.RowWindow(0, 4), P.MineStrategy.BlasFirst, 0, [c2, c1], [])
+    plan = P.CodeletPlan.from_partitions(KernelKind.Spmv, 4, 4, 16, 4, 1, [P.PartitionPlan([g])])
+    x = np.array([1.0, 2.0, 3.0, 4.0])
+    y = np.zeros(4)
+    P.run_spmv(plan, a, x, y, exe)
+    assert bitwise_equal(y, Oracle.run_spmv(plan.export_arrays(), a.view(), x))
+    ctx = P.ExecutionContext(a.values.copy(), x.copy(), np.ones(4))
+    exe.run(plan, ctx, a)  # execute_plan: accumulates onto accum
+    want = np.ones(4) + Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+    assert np.allclose(ctx.accum, want)
