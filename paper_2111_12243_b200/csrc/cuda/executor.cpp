@@ -71,11 +71,11 @@ struct psc_bound {
     int32_t row_begin = 0, row_end = 0, n_rows_total = 0, n_cols = 0;
     int64_t k_begin = 0, k_end = 0;
     bool canonical = true, simple = true;
-    int n_chunks = 0, n_blocks = 0, max_block_rows = 0;
+    int n_chunks = 0, n_blocks = 0, max_block_rows = 0, n_sms = 148;
     int64_t n_segments = 0, long_rows = 0;
     std::string why_general;
     DevBuf ro, col, val;
-    DevBuf rsp, sst, slen, svec, chunk_row, ticket, armed;
+    DevBuf rsp, sst, slen, svec, chunk_row, item_seg, long_list, ticket, armed;
     bool chain_mode = false;
     int max_block_units = 0;
     DevBuf block_row, block_unit, unit_start;
@@ -109,7 +109,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &ticket, &armed, &block_row, &block_unit, &unit_start, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -177,9 +177,12 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->n_segments = static_cast<int64_t>(L.seg_start.size());
         }
         if (p.kernel == PSC_KERNEL_SPMV) {
-            b->chunk_row.upload(L.chunk_row, s);
-            b->n_chunks = static_cast<int>(L.chunk_row.size()) - 1;
+            b->chunk_row.upload(L.items, s);  // warp chunks {r0, r1, k0, k1}
+            b->item_seg.upload(L.item_seg, s);
+            b->long_list.upload(L.long_row_list, s);
+            b->n_chunks = static_cast<int>(L.items.size() / 4);
             b->long_rows = L.long_rows;
+            cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
         } else {
             b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
             b->chain_mode = L.chain_mode;
@@ -256,7 +259,8 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     use_device(b->device);
     if (b->canonical) {
         launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
-                           b->chunk_row.as<int32_t>(), b->n_chunks, b->segs(), false, s);
+                           b->chunk_row.as<int4>(), b->n_chunks, b->item_seg.as<int2>(), b->long_list.as<int32_t>(),
+                           static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, s);
     } else {
         ck(cudaMemsetAsync(y, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset y");
         run_general(b, x, y, nullptr, nullptr, s);
@@ -418,7 +422,7 @@ PSC_API int64_t psc_bound_trace(const psc_bound* b, uint64_t* out, int64_t cap) 
 }
 PSC_API int32_t psc_bound_launches(const psc_bound* b) {
     if (!b) return 0;
-    if (b->canonical) return 1;
+    if (b->canonical) return b->kernel == PSC_KERNEL_SPMV && b->long_rows > 0 && b->n_chunks > 0 ? 2 : 1;
     return static_cast<int32_t>(b->part_group_ptr.size()) - 1;
 }
 PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]) {

@@ -18,10 +18,14 @@ struct SegmentsDev {
 };
 
 // y[r] = (accumulate ? y[r] : 0) + sum of row r's segment partials in plan
-// order, each a 4-lane dot (executor.cpp:23-49). One CTA per chunk.
+// order, each a 4-lane dot (executor.cpp:23-49). items: chunks of short rows
+// {row begin, row end, CSR begin, CSR end} (<= 256 entries and rows each) with
+// their segment ranges item_seg (segmented plans); long_rows: rows with more
+// than 256 entries (kernels.cu "SpMV parity kernels"). Up to two launches.
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
-                        double* y, const int32_t* chunk_row, int n_chunks, SegmentsDev segs,
-                        bool accumulate, cudaStream_t stream);
+                        double* y, const int4* items, int n_items, const int2* item_seg,
+                        const int32_t* long_rows, int n_long, SegmentsDev segs, bool accumulate, int n_sms,
+                        cudaStream_t stream);
 
 // Sync-free blocked triangular solve (kernels.cu, "blocked sync-free
 // triangular solve"): blocks [block_row[i], block_row[i+1]) of rows, solved by

@@ -338,24 +338,30 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
 
     // ---- work units ----
     if (p.kernel == PSC_KERNEL_SPMV) {
-        L.chunk_row.push_back(0);
-        int64_t acc = 0;
+        auto k_of = [&](int32_t r) { return static_cast<int32_t>(ro[r + L.row_begin] - L.k_begin); };
+        auto s_of = [&](int32_t r) { return L.simple ? 0 : L.row_seg_ptr[r]; };
+        int32_t c0 = 0;  // start of the open chunk
+        auto close = [&](int32_t r1) {
+            if (r1 > c0) {
+                L.items.insert(L.items.end(), {c0, r1, k_of(c0), k_of(r1)});
+                L.item_seg.insert(L.item_seg.end(), {s_of(c0), s_of(r1)});
+            }
+        };
         for (int32_t r = 0; r < nr; ++r) {
-            int64_t len = ro[r + L.row_begin + 1] - ro[r + L.row_begin];
-            if (len > kSpmvChunk) {
-                if (L.chunk_row.back() != r) L.chunk_row.push_back(r);
-                L.chunk_row.push_back(r + 1);
-                ++L.long_rows;
-                acc = 0;
+            const int64_t len = ro[r + L.row_begin + 1] - ro[r + L.row_begin];
+            if (len > kSpmvWarpCap) {  // a long row is handled on its own
+                close(r);
+                L.long_row_list.push_back(r);
+                c0 = r + 1;
                 continue;
             }
-            if (acc + len > kSpmvChunk) {
-                L.chunk_row.push_back(r);
-                acc = 0;
+            if (static_cast<int64_t>(k_of(r + 1)) - k_of(c0) > kSpmvWarpCap || r + 1 - c0 > kSpmvWarpCap) {
+                close(r);
+                c0 = r;
             }
-            acc += len;
         }
-        if (L.chunk_row.back() != nr) L.chunk_row.push_back(nr);
+        close(nr);
+        L.long_rows = static_cast<int64_t>(L.long_row_list.size());
     } else {
         // Units: a row continues the unit of the row above when it reads it
         // (its last off-diagonal entry is column r-1).

@@ -36,8 +36,12 @@ struct Lowered {
     std::vector<int32_t> seg_start;  // local CSR position
     std::vector<int32_t> seg_len;
     std::vector<int32_t> seg_vec;  // x index of element 0 when the gather is a unit-stride run, else -1
-    // SpMV work units: chunk boundaries in local rows
-    std::vector<int32_t> chunk_row;
+    // SpMV work in local rows / CSR positions: chunks {r0, r1, k0, k1} of
+    // consecutive short rows (<= kSpmvWarpCap entries and rows), their
+    // segment ranges {s0, s1}, and the rows longer than kSpmvWarpCap
+    std::vector<int32_t> items;     // 4 per chunk
+    std::vector<int32_t> item_seg;  // 2 per chunk (segmented plans)
+    std::vector<int32_t> long_row_list;
     int64_t long_rows = 0;
     // SpTRSV row blocks in local rows, and every block's rows in
     // dependency-level order (the plan's partition index, then row)
@@ -64,7 +68,7 @@ struct Lowered {
     } gen;
 };
 
-constexpr int kSpmvChunk = 2048;  // products staged in shared memory per CTA
+constexpr int kSpmvWarpCap = 256;  // == kWarpCap in kernels.cu
 
 // Lower partitions [part_begin, part_end) (all partitions when part_end < 0).
 // force_general lowers through the exact interpreter even when canonical
