@@ -83,7 +83,7 @@ struct psc_bound {
     DevBuf trace;           // PSC_TRSV_TRACE=1: per-row publish times (diagnostics)
     int trsv_threads = 256; // CTA size of the solve kernel (PSC_TRSV_THREADS)
     int trsv_lat = 700;     // cycles before a lane inspects a load it issued (PSC_TRSV_LAT)
-    bool trsv_lean = false; // lean round kernel: simple rows with <= 4 off-diagonal entries
+    int trsv_lean = 0;      // lean round kernel (simple rows, <= 4 off-diagonal entries): 1 probed, 2 addressed
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
     // general path
     std::vector<int64_t> part_group_ptr;
@@ -206,7 +206,7 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->ticket.ensure(2 * sizeof(int32_t));
             ck(cudaMemsetAsync(b->ticket.p, 0, 2 * sizeof(int32_t), s), "memset");
             if (const char* tr = std::getenv("PSC_TRSV_TRACE"); tr && tr[0] == '1') {
-                const size_t nt = static_cast<size_t>(b->rows()) + b->n_blocks + 1;
+                const size_t nt = static_cast<size_t>(b->rows()) + b->n_blocks + 8;
                 b->trace.ensure(nt * sizeof(unsigned long long));
                 ck(cudaMemsetAsync(b->trace.p, 0, nt * sizeof(unsigned long long), s), "memset");
             }
@@ -215,8 +215,9 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 int32_t max_ext = 0;
                 for (int32_t r = L.row_begin; r < L.row_end; ++r)
                     max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
-                b->trsv_lean = L.simple && max_ext <= 4;
-                if (const char* ln = std::getenv("PSC_TRSV_LEAN")) b->trsv_lean = b->trsv_lean && ln[0] == '1';
+                b->trsv_lean = (L.simple && max_ext <= 4) ? 2 : 0;
+                if (const char* ln = std::getenv("PSC_TRSV_LEAN"))
+                    b->trsv_lean = b->trsv_lean ? std::min(2, std::max(0, std::atoi(ln))) : 0;
             }
             b->armed.ensure(std::max(1, b->n_blocks) * sizeof(int32_t));
             ck(cudaMemsetAsync(b->armed.p, 0, std::max(1, b->n_blocks) * sizeof(int32_t), s), "memset");
@@ -276,7 +277,7 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
                       b->block_row.as<int32_t>(), b->block_unit.as<int32_t>(), b->unit_start.as<int32_t>(), b->n_blocks,
                       b->max_block_rows, b->max_block_units, !b->chain_mode, b->segs(), b->ticket.as<int32_t>(),
                       b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
-                      b->trsv_lean ? -b->trsv_lat : b->trsv_lat, s);
+                      b->trsv_lat, b->trsv_lean, s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");

@@ -38,7 +38,7 @@ void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, con
                    double* acc_out, const int32_t* block_row, const int32_t* block_unit, const int32_t* unit_start,
                    int n_blocks, int max_rows, int max_units, bool single_row_units, SegmentsDev segs,
                    int32_t* ticket, int32_t* armed, int epoch, unsigned long long* trace, int threads,
-                   int poll_latency, cudaStream_t stream);
+                   int poll_latency, int lean, cudaStream_t stream);
 size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units);
 
 // General interpreter (exact Listing-3 semantics) over groups [g0, g1) of one

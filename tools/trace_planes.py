@@ -24,12 +24,13 @@ for _ in range(3):
     bound.sptrsv(b, x)
 torch.cuda.synchronize()
 n, nb = a.n_rows, info["work_units"]
-buf = np.zeros(n + nb + 1, dtype=np.uint64)
+buf = np.zeros(n + nb + 8, dtype=np.uint64)
 _capi.lib().psc_bound_trace(bound._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size)
 t = buf[:n].astype(np.int64)
 t -= t.min()
 T = t.reshape(100, 100, 100)  # z, y, x
-print(f"total {t.max()/1e3:.1f} us, blocks {nb}, block_rows {info['max_block_rows']}")
+st = buf[n + nb:n + nb + 4].astype(float)
+print(f"total {t.max()/1e3:.1f} us, blocks {nb}, block_rows {info['max_block_rows']}; rounds/warp {st[0]/max(st[2],1):.0f}, cycles/round {st[1]/max(st[0],1):.0f} (3 solves)")
 for z in (0, 1, 2, 10, 50, 99):
     print(f"z={z:2d}: (0,0) {T[z,0,0]/1e3:8.1f}  (99,0) {T[z,0,99]/1e3:8.1f}  (0,99) {T[z,99,0]/1e3:8.1f}  "
           f"(99,99) {T[z,99,99]/1e3:8.1f} us")

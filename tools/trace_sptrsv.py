@@ -27,10 +27,12 @@ for _ in range(3):
 torch.cuda.synchronize()
 n = a.n_rows
 nb = info["work_units"]
-buf = np.zeros(n + nb + 1, dtype=np.uint64)
+buf = np.zeros(n + nb + 8, dtype=np.uint64)
 got = _capi.lib().psc_bound_trace(bound._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size)
-assert got == n + nb + 1, got
-rounds = int(buf[n + nb]); buf = buf[:n + nb]
+assert got == n + nb + 8, got
+stats = buf[n + nb:n + nb + 4].astype(np.float64); buf = buf[:n + nb]
+rounds = stats[0]
+print(f'warps {stats[2]:.0f} rounds/warp {stats[0]/max(stats[2],1):.0f} cycles/round {stats[1]/max(stats[0],1):.0f} rows {stats[3]:.0f} (3 solves accumulated)')
 t_rows = buf[:n].astype(np.int64)
 t_arm = buf[n:].astype(np.int64)
 t0 = t_arm.min()
