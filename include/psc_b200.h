@@ -204,6 +204,12 @@ PSC_API int32_t psc_bound_launches(const psc_bound* b);
  * path (0 parity-segments, 1 general interpreter), algorithmic bytes per call
  * (DESIGN.md), device bytes held, long rows, reserved. */
 PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]);
+/* Diagnostic: count mismatches between the solve kernels' division (exact
+ * reciprocal refinement + final correction, __ddiv_rn outside exponents
+ * [-500, 500]) and IEEE division on n random operand pairs whose exponents
+ * lie in [-exp_span, exp_span]. Replaces no reference interface. */
+PSC_API psc_status psc_selftest_division(uint64_t seed, int64_t n, int32_t exp_span, int64_t* mismatches);
+
 PSC_API int32_t psc_device_count(void);
 
 /* Host-span entry points with the reference's contracts (executor.cpp:274-308):

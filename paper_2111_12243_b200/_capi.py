@@ -175,6 +175,7 @@ _SIGS = {
     "psc_uniform_vector": (None, [c_int64, c_uint64, c_double, c_double, POINTER(c_double)]),
     "psc_int_vector": (None, [c_int64, c_uint64, POINTER(c_double)]),
     "psc_device_count": (c_int32, []),
+    "psc_selftest_division": (c_int32, [C.c_uint64, c_int64, c_int32, C.POINTER(c_int64)]),
 }
 
 _lib = None

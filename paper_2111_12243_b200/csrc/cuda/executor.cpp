@@ -83,7 +83,11 @@ struct psc_bound {
     DevBuf trace;           // PSC_TRSV_TRACE=1: per-row publish times (diagnostics)
     int trsv_threads = 256; // CTA size of the solve kernel (PSC_TRSV_THREADS)
     int trsv_lat = 700;     // cycles before a lane inspects a load it issued (PSC_TRSV_LAT)
-    int trsv_lean = 0;      // lean round kernel (simple rows, <= 4 off-diagonal entries): 1 probed, 2 addressed
+    int trsv_lean = 0;      // round kernel for simple rows with <= 4 off-diagonal entries: 1 probed, 2 records
+    DevBuf rec;             // trsv_lean == 2: per-row records (trsv_pack_kernel)
+    DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, sx slot)
+    bool tiled = false;     // blocks grown over the unit graph (not row ranges)
+    bool rec_dirty = true;  // values changed since the records were packed
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
     // general path
     std::vector<int64_t> part_group_ptr;
@@ -109,7 +113,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &unit_len, &unit_loc, &row_block, &row_loc, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -184,12 +188,57 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->long_rows = L.long_rows;
             cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
         } else {
+            // Solve-round kernel: records (lean 2) for simple rows with <= 4
+            // off-diagonal entries, <= 2 of them in other blocks; probed rounds
+            // (lean 1) for other simple short rows; generic rounds otherwise.
+            // Record kernels in chain mode take tiled blocks (tile_chain_blocks).
+            int32_t max_ext = 0;
+            for (int32_t r = L.row_begin; r < L.row_end; ++r)
+                max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
+            const bool lean = L.simple && max_ext <= 4;
+            int want = lean ? 2 : 0;
+            if (const char* ln = std::getenv("PSC_TRSV_LEAN")) want = std::min(want, std::max(0, std::atoi(ln)));
+            auto recs_ok = [&](const Lowered& M) {
+                if (M.max_block_rows > 32767) return false;
+                for (int32_t r = M.row_begin; r < M.row_end; ++r) {
+                    int g = 0;
+                    for (int32_t k = a.row_offsets[r]; k < a.row_offsets[r + 1] - 1; ++k)
+                        g += M.row_block[a.col_indices[k]] != M.row_block[r];
+                    if (g > 2) return false;
+                }
+                return true;
+            };
+            b->trsv_lean = lean ? 1 : 0;
+            if (want == 2) {
+                bool tiles = L.chain_mode;
+                if (const char* tv = std::getenv("PSC_TRSV_TILES")) tiles = tiles && tv[0] != '0';
+                if (tiles) {
+                    Lowered T = L;
+                    if (tile_chain_blocks(T, a, L.max_block_rows) && recs_ok(T)) {
+                        L = std::move(T);
+                        b->trsv_lean = 2;
+                    }
+                }
+                if (b->trsv_lean != 2) {
+                    unit_maps(L);
+                    if (recs_ok(L)) b->trsv_lean = 2;
+                }
+            }
+            if (want < b->trsv_lean) b->trsv_lean = want;
             b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
             b->chain_mode = L.chain_mode;
+            b->tiled = L.tiled;
             b->block_row.upload(L.block_row, s);
             b->block_unit.upload(L.block_unit, s);
             b->unit_start.upload(L.unit_start, s);
             b->max_block_units = L.max_block_units;
+            if (b->trsv_lean == 2) {
+                b->unit_len.upload(L.unit_len, s);
+                b->unit_loc.upload(L.unit_loc, s);
+                b->row_block.upload(L.row_block, s);
+                b->row_loc.upload(L.row_loc, s);
+                b->rec.ensure(static_cast<size_t>(b->rows()) * trsv_rec_bytes());
+            }
             // CTA size: enough lanes for the units of a block (chain mode) or
             // 256 (row mode), within the shared-memory budget
             int th = 256;
@@ -198,6 +247,11 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 while (th < 512 && th < L.max_block_units) th *= 2;
             }
             if (const char* env = std::getenv("PSC_TRSV_THREADS")) th = std::atoi(env);
+            {   // the solve kernels are instantiated for 64, 128, 256 and 512 threads
+                int p = 64;
+                while (p < 512 && p < th) p *= 2;
+                th = p;
+            }
             auto smem_of = [&](int t) { return sptrsv_smem_bytes(t, L.max_block_rows, L.max_block_units); };
             while (th > 64 && smem_of(th) > 232448) th /= 2;
             require(smem_of(th) <= 232448, "bind: solve block does not fit in shared memory");
@@ -211,14 +265,6 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 ck(cudaMemsetAsync(b->trace.p, 0, nt * sizeof(unsigned long long), s), "memset");
             }
             if (const char* tl = std::getenv("PSC_TRSV_LAT")) b->trsv_lat = std::atoi(tl);
-            {
-                int32_t max_ext = 0;
-                for (int32_t r = L.row_begin; r < L.row_end; ++r)
-                    max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
-                b->trsv_lean = (L.simple && max_ext <= 4) ? 2 : 0;
-                if (const char* ln = std::getenv("PSC_TRSV_LEAN"))
-                    b->trsv_lean = b->trsv_lean ? std::min(2, std::max(0, std::atoi(ln))) : 0;
-            }
             b->armed.ensure(std::max(1, b->n_blocks) * sizeof(int32_t));
             ck(cudaMemsetAsync(b->armed.p, 0, std::max(1, b->n_blocks) * sizeof(int32_t), s), "memset");
         }
@@ -272,12 +318,18 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
 void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s) {
     use_device(b->device);
     if (b->canonical) {
+        if (b->trsv_lean == 2 && b->rec_dirty) {
+            launch_trsv_pack(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), b->row_block.as<int32_t>(),
+                             b->row_loc.as<int32_t>(), b->rows(), b->rec.p, s);
+            b->rec_dirty = false;
+        }
         b->epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;
         launch_sptrsv(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,
                       b->block_row.as<int32_t>(), b->block_unit.as<int32_t>(), b->unit_start.as<int32_t>(), b->n_blocks,
                       b->max_block_rows, b->max_block_units, !b->chain_mode, b->segs(), b->ticket.as<int32_t>(),
                       b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
-                      b->trsv_lat, b->trsv_lean, s);
+                      b->trsv_lat, b->trsv_lean, b->rec.p, b->unit_len.as<int32_t>(),
+                      b->unit_loc.as<int32_t>(), s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");
@@ -301,6 +353,15 @@ psc_bound* cached_bound(psc_executor* e, const psc_plan* plan, const psc_csr_vie
 }  // namespace pscb
 
 extern "C" {
+
+PSC_API psc_status psc_selftest_division(uint64_t seed, int64_t n, int32_t exp_span, int64_t* mismatches) {
+    return guarded([&] {
+        require(mismatches != nullptr && n >= 0 && exp_span >= 1 && exp_span <= 1000, "selftest_division: bad argument");
+        const int64_t m = division_selftest(seed, n, exp_span);
+        require(m >= 0, "selftest_division: CUDA error");
+        *mismatches = m;
+    });
+}
 
 PSC_API int32_t psc_device_count(void) {
     int n = 0;
@@ -485,6 +546,7 @@ PSC_API psc_status psc_run_sptrsv(psc_executor* e, const psc_plan* plan, const p
         cudaStream_t s = e->stream;
         use_device(e->device);
         b->val.upload_raw(l->values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);
+        b->rec_dirty = true;
         size_t bytes = std::max<int64_t>(n, 1) * sizeof(double);
         e->vb.upload_raw(rhs, n * sizeof(double), s);
         e->vx.ensure(bytes);
@@ -513,6 +575,7 @@ PSC_API psc_status psc_execute_plan(psc_executor* e, const psc_plan* plan, const
         use_device(e->device);
         const int64_t n = a->n_rows, nc = a->n_cols;
         b->val.upload_raw(ctx->matrix_values, a->nnz * sizeof(double), s);
+        b->rec_dirty = true;
         e->vy.upload_raw(ctx->accum, n * sizeof(double), s);
         if (solve) {
             // gather aliases solution (executor.hpp:12-23)

@@ -425,6 +425,152 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
     return L;
 }
 
+void unit_maps(Lowered& L) {
+    const int32_t nr = L.row_end - L.row_begin;
+    const size_t nu = L.unit_start.size();
+    L.unit_len.assign(nu, 1);
+    L.unit_loc.assign(nu, 0);
+    L.row_block.assign(nr, 0);
+    L.row_loc.assign(nr, 0);
+    for (size_t bi = 0; bi + 1 < L.block_row.size(); ++bi) {
+        const int32_t b0 = L.block_row[bi], b1 = L.block_row[bi + 1];
+        for (int32_t r = b0; r < b1; ++r) {
+            L.row_block[r] = static_cast<int32_t>(bi);
+            L.row_loc[r] = r - b0;
+        }
+        const int32_t u0 = L.block_unit[bi], u1 = L.block_unit[bi + 1];
+        for (int32_t u = u0; u < u1; ++u) {
+            L.unit_loc[u] = L.unit_start[u] - b0;
+            if (L.chain_mode) L.unit_len[u] = (u + 1 < u1 ? L.unit_start[u + 1] : b1) - L.unit_start[u];
+        }
+    }
+    L.tiled = false;
+}
+
+bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows) {
+    if (!L.chain_mode || L.row_begin != 0) return false;
+    const int32_t nr = L.row_end;
+    unit_maps(L);  // contiguous unit lengths
+    const int32_t nu = static_cast<int32_t>(L.unit_start.size());
+    if (nu < 2) return false;
+    std::vector<int32_t> start(L.unit_start), len(L.unit_len);
+    std::vector<int32_t> unit_of(nr);
+    for (int32_t u = 0; u < nu; ++u)
+        for (int32_t r = start[u]; r < start[u] + len[u]; ++r) unit_of[r] = u;
+    // dependency lists (deduplicated) and dependents
+    std::vector<int64_t> dep_ptr(nu + 1, 0);
+    std::vector<int32_t> deps;
+    std::vector<int32_t> seen(nu, -1);
+    for (int32_t u = 0; u < nu; ++u) {
+        for (int32_t r = start[u]; r < start[u] + len[u]; ++r) {
+            for (int64_t k = a.row_offsets[r]; k < a.row_offsets[r + 1] - 1; ++k) {
+                const int32_t v = unit_of[a.col_indices[k]];
+                if (v != u && seen[v] != u) {
+                    seen[v] = u;
+                    deps.push_back(v);
+                }
+            }
+        }
+        dep_ptr[u + 1] = static_cast<int64_t>(deps.size());
+    }
+    std::vector<int64_t> out_ptr(nu + 1, 0);
+    for (int32_t v : deps) ++out_ptr[v + 1];
+    for (int32_t u = 0; u < nu; ++u) out_ptr[u + 1] += out_ptr[u];
+    std::vector<int32_t> outs(deps.size());
+    {
+        std::vector<int64_t> fill(out_ptr.begin(), out_ptr.end() - 1);
+        for (int32_t u = 0; u < nu; ++u)
+            for (int64_t k = dep_ptr[u]; k < dep_ptr[u + 1]; ++k) outs[fill[deps[k]]++] = u;
+    }
+    std::vector<int32_t> remaining(nu), block_of(nu, -1), affinity(nu, 0);
+    // ready units: `pool` (FIFO by discovery, affinity to earlier blocks only)
+    // and `heap` (became ready while the open block grew: (affinity, -order))
+    std::vector<int32_t> pool;
+    size_t pool_head = 0;
+    std::vector<std::pair<std::pair<int32_t, int64_t>, int32_t>> heap;
+    int64_t order = 0;
+    std::vector<int64_t> disc(nu, 0);
+    for (int32_t u = 0; u < nu; ++u) {
+        remaining[u] = static_cast<int32_t>(dep_ptr[u + 1] - dep_ptr[u]);
+        if (remaining[u] == 0) {
+            disc[u] = order++;
+            pool.push_back(u);
+        }
+    }
+    std::vector<int32_t> new_unit_start, new_block_unit{0}, new_block_row{0}, new_len;
+    int32_t cur_block = 0, cur_rows = 0, placed = 0;
+    auto close_block = [&] {
+        if (cur_rows == 0) return;
+        new_block_unit.push_back(static_cast<int32_t>(new_unit_start.size()));
+        new_block_row.push_back(new_block_row.back() + cur_rows);
+        ++cur_block;
+        cur_rows = 0;
+        for (auto& e : heap) pool.push_back(e.second);  // no affinity to the next block
+        heap.clear();
+    };
+    while (placed < nu) {
+        int32_t u = -1;
+        if (!heap.empty()) {
+            std::pop_heap(heap.begin(), heap.end());
+            u = heap.back().second;
+            heap.pop_back();
+        } else {
+            while (pool_head < pool.size() && block_of[pool[pool_head]] >= 0) ++pool_head;
+            if (pool_head == pool.size()) return false;  // cycle: not a triangle
+            u = pool[pool_head++];
+        }
+        if (block_of[u] >= 0) continue;
+        if (cur_rows > 0 && cur_rows + len[u] > max_rows) {
+            close_block();
+            // u has no affinity to the new block; it seeds it
+        }
+        block_of[u] = cur_block;
+        new_unit_start.push_back(start[u]);
+        new_len.push_back(len[u]);
+        cur_rows += len[u];
+        ++placed;
+        for (int64_t k = out_ptr[u]; k < out_ptr[u + 1]; ++k) {
+            const int32_t w = outs[k];
+            ++affinity[w];
+            if (--remaining[w] == 0) {
+                disc[w] = order++;
+                // affinity = dependencies of w inside the open block
+                int32_t in = 0;
+                for (int64_t j = dep_ptr[w]; j < dep_ptr[w + 1]; ++j) in += block_of[deps[j]] == cur_block;
+                heap.push_back({{in, -disc[w]}, w});
+                std::push_heap(heap.begin(), heap.end());
+            }
+        }
+    }
+    close_block();
+    // adopt the tiled layout
+    const int32_t nb = static_cast<int32_t>(new_block_row.size()) - 1;
+    L.unit_start = std::move(new_unit_start);
+    L.unit_len = std::move(new_len);
+    L.block_unit = std::move(new_block_unit);
+    L.block_row = std::move(new_block_row);
+    L.unit_loc.assign(L.unit_start.size(), 0);
+    L.row_block.assign(nr, 0);
+    L.row_loc.assign(nr, 0);
+    L.max_block_rows = 0;
+    L.max_block_units = 0;
+    for (int32_t bi = 0; bi < nb; ++bi) {
+        int32_t loc = 0;
+        for (int32_t u = L.block_unit[bi]; u < L.block_unit[bi + 1]; ++u) {
+            L.unit_loc[u] = loc;
+            for (int32_t j = 0; j < L.unit_len[u]; ++j) {
+                L.row_block[L.unit_start[u] + j] = bi;
+                L.row_loc[L.unit_start[u] + j] = loc + j;
+            }
+            loc += L.unit_len[u];
+        }
+        L.max_block_rows = std::max(L.max_block_rows, loc);
+        L.max_block_units = std::max(L.max_block_units, L.block_unit[bi + 1] - L.block_unit[bi]);
+    }
+    L.tiled = true;
+    return true;
+}
+
 Lowered lower_single_codelet(const psc_codelet_view& cv, int which) {
     check_codelet_shape(which, cv.out.form, cv.mat.form, cv.vec.form);
     Plan p;

@@ -53,6 +53,12 @@ struct Lowered {
     std::vector<int32_t> unit_start, block_unit;
     int32_t max_block_units = 0;
     int32_t max_block_rows = 0;
+    // record kernel layout (unit_maps / tile_chain_blocks): every unit's row
+    // count and first shared-memory slot in its block, every row's block and
+    // slot. block_row then holds the prefix sum of block sizes; with tiled
+    // blocks it no longer delimits row ranges.
+    std::vector<int32_t> unit_len, unit_loc, row_block, row_loc;
+    bool tiled = false;
     std::string why_general;  // reason the plan is not canonical
 
     // general interpreter tables (only when !canonical)
@@ -75,6 +81,19 @@ constexpr int kSpmvWarpCap = 256;  // == kWarpCap in kernels.cu
 // (execute_plan accumulates onto caller-provided accum/solution arrays).
 Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int64_t part_end,
                    int sptrsv_block_rows, bool force_general = false);
+
+// Fill unit_len / unit_loc / row_block / row_loc for the contiguous blocks
+// lower_plan produced (SpTRSV).
+void unit_maps(Lowered& L);
+
+// Chain mode: regroup units into blocks of <= max_rows rows grown greedily
+// over the unit dependency graph (a unit joins the open block once all its
+// dependencies are placed, preferring the unit with most dependencies inside
+// the open block, then discovery order), so blocks are compact regions and a
+// dependency chain crosses few block boundaries. Blocks stay topologically
+// ordered. Fills the record-kernel maps; returns false (L unchanged) when not
+// applicable.
+bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows);
 
 // Build a general-path lowering of one hand-built codelet (exec_*_codelet).
 Lowered lower_single_codelet(const psc_codelet_view& c, int which);

@@ -196,3 +196,50 @@ def test_general_path_hand_built_plan(exe):
     exe.run(plan, ctx, a)  # execute_plan: accumulates onto accum
     want = np.ones(4) + Oracle.run_spmv(plan.export_arrays(), a.view(), x)
     assert np.allclose(ctx.accum, want)
+
+
+def test_division_matches_ieee():
+    """The solve kernels divide with a precomputed reciprocal and the final
+    correction of the IEEE division (kernels.cu div_with_rcp); it must agree
+    bitwise with __ddiv_rn everywhere, including the fallback range."""
+    from paper_2111_12243_b200 import _capi
+    import ctypes as C
+    for seed, span in ((1, 60), (2, 500), (3, 1000)):
+        bad = C.c_int64(-1)
+        st = _capi.lib().psc_selftest_division(seed, 20_000_000, span, C.byref(bad))
+        assert st == 0, _capi.lib().psc_last_error()
+        assert bad.value == 0, (span, bad.value)
+
+
+@pytest.mark.parametrize("lean", ["0", "1", "2"])
+@pytest.mark.parametrize("block_rows", ["1024", "0"])
+def test_sptrsv_round_kernels_bitwise(monkeypatch, lean, block_rows):
+    """Every solve-round kernel (generic, probed, record-driven), with default
+    and small blocks (many operands from earlier blocks), equals the oracle."""
+    monkeypatch.setenv("PSC_TRSV_LEAN", lean)
+    if block_rows != "0":
+        monkeypatch.setenv("PSC_SPTRSV_BLOCK_ROWS", block_rows)
+    for config, scale in ((2, 0.03), (4, 0.02), (3, 0.01), (1, 0.002)):
+        a = P.generate_config(config, scale)
+        if config in (1, 3):  # SpMV matrices: solve with their lower triangle
+            a = P.lower_triangular(a).csr()
+        plan = P.inspect(KernelKind.Sptrsv, a, 3, 8)
+        b = P.uniform_vector(a.n_rows, 5)
+        exe = P.Executor(1)
+        got = run_gpu(exe, plan, KernelKind.Sptrsv, a, b)
+        want = run_oracle(plan, KernelKind.Sptrsv, a, b)
+        assert bitwise_equal(got, want), (config, lean, block_rows)
+
+
+def test_sptrsv_value_update_repacks(exe):
+    """run_sptrsv re-uploads values on every call (the reference reads them
+    live); the per-row records must follow."""
+    a = P.generate_config(2, 0.03)
+    plan = P.inspect(KernelKind.Sptrsv, a, 3, 8)
+    b = P.uniform_vector(a.n_rows, 9)
+    first = run_gpu(exe, plan, KernelKind.Sptrsv, a, b)
+    assert bitwise_equal(first, run_oracle(plan, KernelKind.Sptrsv, a, b))
+    a.values[:] = a.values * 0.5 + 0.25
+    second = run_gpu(exe, plan, KernelKind.Sptrsv, a, b)
+    assert bitwise_equal(second, run_oracle(plan, KernelKind.Sptrsv, a, b))
+    assert not bitwise_equal(first, second)

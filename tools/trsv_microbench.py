@@ -37,7 +37,7 @@ def run(a, label, reps=20):
 chain = P.banded(8192, 1, True)
 for v in range(chain.nnz()):
     chain.values[v] = 1.0 if chain.col_indices[v] == np.searchsorted(chain.row_offsets, v, "right") - 1 else 0.5
-for T in (32, 128, 512):
+for T in (64, 128, 512):
     os.environ["PSC_TRSV_THREADS"] = str(T)
     os.environ["PSC_SPTRSV_BLOCK_ROWS"] = "8192"
     run(chain, f"bidiagonal 8192, 1 block, T={T}")
