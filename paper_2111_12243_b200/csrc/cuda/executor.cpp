@@ -85,7 +85,9 @@ struct psc_bound {
     int trsv_lat = 700;     // cycles before a lane inspects a load it issued (PSC_TRSV_LAT)
     int trsv_lean = 0;      // round kernel for simple rows with <= 4 off-diagonal entries: 1 probed, 2 records
     DevBuf rec;             // trsv_lean == 2: per-row records (trsv_pack_kernel)
-    DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, sx slot)
+    DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, window slot)
+    DevBuf halo_ptr, halo_col, halo_key, halo_pos;  // trsv_lean == 2: per block, the x entries it reads from earlier blocks
+    int max_block_halo = -1;
     bool tiled = false;     // blocks grown over the unit graph (not row ranges)
     bool rec_dirty = true;  // values changed since the records were packed
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
@@ -113,7 +115,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &unit_len, &unit_loc, &row_block, &row_loc, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &unit_len, &unit_loc, &row_block, &row_loc, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -189,24 +191,32 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
         } else {
             // Solve-round kernel: records (lean 2) for simple rows with <= 4
-            // off-diagonal entries, <= 2 of them in other blocks; probed rounds
-            // (lean 1) for other simple short rows; generic rounds otherwise.
-            // Record kernels in chain mode take tiled blocks (tile_chain_blocks).
+            // off-diagonal entries whose block window (rows + halo) fits in
+            // shared memory; probed rounds (lean 1) for other simple short
+            // rows; generic rounds otherwise. Record kernels in chain mode take
+            // tiled blocks (tile_chain_blocks).
             int32_t max_ext = 0;
             for (int32_t r = L.row_begin; r < L.row_end; ++r)
                 max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
             const bool lean = L.simple && max_ext <= 4;
             int want = lean ? 2 : 0;
             if (const char* ln = std::getenv("PSC_TRSV_LEAN")) want = std::min(want, std::max(0, std::atoi(ln)));
-            auto recs_ok = [&](const Lowered& M) {
-                if (M.max_block_rows > 32767) return false;
-                for (int32_t r = M.row_begin; r < M.row_end; ++r) {
-                    int g = 0;
-                    for (int32_t k = a.row_offsets[r]; k < a.row_offsets[r + 1] - 1; ++k)
-                        g += M.row_block[a.col_indices[k]] != M.row_block[r];
-                    if (g > 2) return false;
+            auto pick_threads = [&](const Lowered& M, int max_halo) {
+                int th = 256;
+                if (M.chain_mode) {  // enough lanes for the units of a block
+                    th = 64;
+                    while (th < 512 && th < M.max_block_units) th *= 2;
                 }
-                return true;
+                if (const char* env = std::getenv("PSC_TRSV_THREADS")) th = std::atoi(env);
+                int p2 = 64;  // the solve kernels are instantiated for 64, 128, 256 and 512 threads
+                while (p2 < 512 && p2 < th) p2 *= 2;
+                th = p2;
+                while (th > 64 && sptrsv_smem_bytes(th, M.max_block_rows, M.max_block_units, max_halo) > 232448) th /= 2;
+                return sptrsv_smem_bytes(th, M.max_block_rows, M.max_block_units, max_halo) <= 232448 ? th : -1;
+            };
+            auto recs_fit = [&](Lowered& M) {  // window indices fit int16 and the window fits
+                block_halos(M, a);
+                return M.max_block_rows + M.max_block_halo <= 32767 && pick_threads(M, M.max_block_halo) > 0;
             };
             b->trsv_lean = lean ? 1 : 0;
             if (want == 2) {
@@ -214,14 +224,18 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 if (const char* tv = std::getenv("PSC_TRSV_TILES")) tiles = tiles && tv[0] != '0';
                 if (tiles) {
                     Lowered T = L;
-                    if (tile_chain_blocks(T, a, L.max_block_rows) && recs_ok(T)) {
+                    if (tile_chain_blocks(T, a, L.max_block_rows) && recs_fit(T)) {
                         L = std::move(T);
                         b->trsv_lean = 2;
                     }
                 }
                 if (b->trsv_lean != 2) {
-                    unit_maps(L);
-                    if (recs_ok(L)) b->trsv_lean = 2;
+                    Lowered C = L;
+                    unit_maps(C);
+                    if (recs_fit(C)) {
+                        L = std::move(C);
+                        b->trsv_lean = 2;
+                    }
                 }
             }
             if (want < b->trsv_lean) b->trsv_lean = want;
@@ -232,29 +246,21 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->block_unit.upload(L.block_unit, s);
             b->unit_start.upload(L.unit_start, s);
             b->max_block_units = L.max_block_units;
+            b->max_block_halo = -1;
             if (b->trsv_lean == 2) {
                 b->unit_len.upload(L.unit_len, s);
                 b->unit_loc.upload(L.unit_loc, s);
                 b->row_block.upload(L.row_block, s);
                 b->row_loc.upload(L.row_loc, s);
+                b->halo_ptr.upload(L.halo_ptr, s);
+                b->halo_col.upload(L.halo_col, s);
+                b->halo_key.upload(L.halo_key, s);
+                b->halo_pos.upload(L.halo_pos, s);
+                b->max_block_halo = L.max_block_halo;
                 b->rec.ensure(static_cast<size_t>(b->rows()) * trsv_rec_bytes());
             }
-            // CTA size: enough lanes for the units of a block (chain mode) or
-            // 256 (row mode), within the shared-memory budget
-            int th = 256;
-            if (L.chain_mode) {
-                th = 64;
-                while (th < 512 && th < L.max_block_units) th *= 2;
-            }
-            if (const char* env = std::getenv("PSC_TRSV_THREADS")) th = std::atoi(env);
-            {   // the solve kernels are instantiated for 64, 128, 256 and 512 threads
-                int p = 64;
-                while (p < 512 && p < th) p *= 2;
-                th = p;
-            }
-            auto smem_of = [&](int t) { return sptrsv_smem_bytes(t, L.max_block_rows, L.max_block_units); };
-            while (th > 64 && smem_of(th) > 232448) th /= 2;
-            require(smem_of(th) <= 232448, "bind: solve block does not fit in shared memory");
+            const int th = pick_threads(L, b->max_block_halo);
+            require(th > 0, "bind: solve block does not fit in shared memory");
             b->trsv_threads = th;
             b->max_block_rows = L.max_block_rows;
             b->ticket.ensure(2 * sizeof(int32_t));
@@ -320,7 +326,8 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
     if (b->canonical) {
         if (b->trsv_lean == 2 && b->rec_dirty) {
             launch_trsv_pack(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), b->row_block.as<int32_t>(),
-                             b->row_loc.as<int32_t>(), b->rows(), b->rec.p, s);
+                             b->row_loc.as<int32_t>(), b->block_row.as<int32_t>(), b->halo_ptr.as<int32_t>(),
+                             b->halo_key.as<int32_t>(), b->halo_pos.as<int32_t>(), b->rows(), b->rec.p, s);
             b->rec_dirty = false;
         }
         b->epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;
@@ -329,7 +336,7 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
                       b->max_block_rows, b->max_block_units, !b->chain_mode, b->segs(), b->ticket.as<int32_t>(),
                       b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
                       b->trsv_lat, b->trsv_lean, b->rec.p, b->unit_len.as<int32_t>(),
-                      b->unit_loc.as<int32_t>(), s);
+                      b->unit_loc.as<int32_t>(), b->halo_ptr.as<int32_t>(), b->halo_col.as<int32_t>(), b->max_block_halo, s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");

@@ -39,13 +39,15 @@ void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, con
                    int n_blocks, int max_rows, int max_units, bool single_row_units, SegmentsDev segs,
                    int32_t* ticket, int32_t* armed, int epoch, unsigned long long* trace, int threads,
                    int poll_latency, int lean, const void* rec, const int32_t* unit_len,
-                   const int32_t* unit_loc, cudaStream_t stream);
+                   const int32_t* unit_loc, const int32_t* halo_ptr, const int32_t* halo_col, int max_halo,
+                   cudaStream_t stream);
 size_t trsv_rec_bytes();
 void launch_trsv_pack(const int32_t* ro, const int32_t* col, const double* val, const int32_t* row_block,
-                      const int32_t* row_loc, int n_rows, void* rec, cudaStream_t stream);
+                      const int32_t* row_loc, const int32_t* block_row, const int32_t* halo_ptr, const int32_t* halo_key,
+                      const int32_t* halo_pos, int n_rows, void* rec, cudaStream_t stream);
 // mismatches between the record kernel's division and __ddiv_rn on n random operand pairs (-1: CUDA error)
 int64_t division_selftest(uint64_t seed, int64_t n, int exp_span);
-size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units);
+size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units, int max_halo = -1);  // max_halo >= 0: record kernel
 
 // General interpreter (exact Listing-3 semantics) over groups [g0, g1) of one
 // partition; one thread per region group.

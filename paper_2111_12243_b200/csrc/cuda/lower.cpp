@@ -571,6 +571,58 @@ bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows) {
     return true;
 }
 
+void block_halos(Lowered& L, const psc_csr_view& a) {
+    const int32_t nb = static_cast<int32_t>(L.block_row.size()) - 1;
+    const int32_t nr = L.row_end - L.row_begin;
+    // dependency level of every row (longest path from a row without
+    // off-diagonal entries): the halo is listed in the order its entries are
+    // produced, so the halo warp's lanes rarely wait behind a late entry
+    std::vector<int32_t> lvl(nr, 0);
+    for (int32_t r = 0; r < nr; ++r) {
+        const int32_t gr = r + L.row_begin;
+        int32_t m = -1;
+        for (int64_t k = a.row_offsets[gr]; k < a.row_offsets[gr + 1] - 1; ++k) {
+            const int32_t c = a.col_indices[k] - L.row_begin;
+            if (c >= 0 && c < r) m = std::max(m, lvl[c]);
+        }
+        lvl[r] = m + 1;
+    }
+    L.halo_ptr.assign(1, 0);
+    L.halo_col.clear();
+    L.halo_key.clear();
+    L.halo_pos.clear();
+    L.max_block_halo = 0;
+    std::vector<int32_t> cols, pos;
+    for (int32_t bi = 0; bi < nb; ++bi) {
+        cols.clear();
+        for (int32_t u = L.block_unit[bi]; u < L.block_unit[bi + 1]; ++u) {
+            for (int32_t r = L.unit_start[u]; r < L.unit_start[u] + L.unit_len[u]; ++r) {
+                const int32_t gr = r + L.row_begin;
+                for (int64_t k = a.row_offsets[gr]; k < a.row_offsets[gr + 1] - 1; ++k) {
+                    const int32_t c = a.col_indices[k];
+                    if (L.row_block[c - L.row_begin] != bi) cols.push_back(c);
+                }
+            }
+        }
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        L.halo_key.insert(L.halo_key.end(), cols.begin(), cols.end());  // by column, for lookups
+        pos.resize(cols.size());
+        for (size_t i = 0; i < cols.size(); ++i) pos[i] = static_cast<int32_t>(i);
+        std::stable_sort(pos.begin(), pos.end(), [&](int32_t p, int32_t q) {
+            return lvl[cols[p] - L.row_begin] < lvl[cols[q] - L.row_begin];
+        });
+        std::vector<int32_t> where(cols.size());
+        for (size_t i = 0; i < pos.size(); ++i) {
+            L.halo_col.push_back(cols[pos[i]]);
+            where[pos[i]] = static_cast<int32_t>(i);
+        }
+        L.halo_pos.insert(L.halo_pos.end(), where.begin(), where.end());
+        L.halo_ptr.push_back(static_cast<int32_t>(L.halo_col.size()));
+        L.max_block_halo = std::max(L.max_block_halo, static_cast<int32_t>(cols.size()));
+    }
+}
+
 Lowered lower_single_codelet(const psc_codelet_view& cv, int which) {
     check_codelet_shape(which, cv.out.form, cv.mat.form, cv.vec.form);
     Plan p;

@@ -59,6 +59,11 @@ struct Lowered {
     // blocks it no longer delimits row ranges.
     std::vector<int32_t> unit_len, unit_loc, row_block, row_loc;
     bool tiled = false;
+    // per block: the distinct columns it reads from other blocks (sorted),
+    // mirrored into shared memory after the block's own rows (block_halos)
+    std::vector<int32_t> halo_ptr, halo_col;  // halo_col: in production (level) order
+    std::vector<int32_t> halo_key, halo_pos;  // the same columns sorted, and their halo_col positions
+    int32_t max_block_halo = 0;
     std::string why_general;  // reason the plan is not canonical
 
     // general interpreter tables (only when !canonical)
@@ -94,6 +99,10 @@ void unit_maps(Lowered& L);
 // ordered. Fills the record-kernel maps; returns false (L unchanged) when not
 // applicable.
 bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows);
+
+// Fill halo_ptr / halo_col / max_block_halo from row_block (after unit_maps
+// or tile_chain_blocks).
+void block_halos(Lowered& L, const psc_csr_view& a);
 
 // Build a general-path lowering of one hand-built codelet (exec_*_codelet).
 Lowered lower_single_codelet(const psc_codelet_view& c, int which);
