@@ -321,7 +321,7 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     ck(cudaGetLastError(), "spmv launch");
 }
 
-void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s) {
+void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s, double* x_host = nullptr) {
     use_device(b->device);
     if (b->canonical) {
         if (b->trsv_lean == 2 && b->rec_dirty) {
@@ -336,7 +336,8 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
                       b->max_block_rows, b->max_block_units, !b->chain_mode, b->segs(), b->ticket.as<int32_t>(),
                       b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
                       b->trsv_lat, b->trsv_lean, b->rec.p, b->unit_len.as<int32_t>(),
-                      b->unit_loc.as<int32_t>(), b->halo_ptr.as<int32_t>(), b->halo_col.as<int32_t>(), b->max_block_halo, s);
+                      b->unit_loc.as<int32_t>(), b->halo_ptr.as<int32_t>(), b->halo_col.as<int32_t>(), b->max_block_halo,
+                      b->trsv_lean == 2 ? x_host : nullptr, s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");
@@ -473,8 +474,20 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
         b->hx.ensure(std::max<size_t>(bytes, 8));
         if (!b->canonical) b->hx.upload_raw(x, bytes, s);
         if (acc || !b->canonical) b->hacc.ensure(std::max<size_t>(bytes, 8));
-        bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), (acc || !b->canonical) ? b->hacc.as<double>() : nullptr, s);
-        ck(cudaMemcpyAsync(x, b->hx.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+        // A pinned, mapped x (UVA) is written by the record kernel directly:
+        // every finished chain unit is shipped by one bulk copy, overlapping
+        // the solve instead of a copy after it.
+        double* x_map = nullptr;
+        if (b->canonical && b->trsv_lean == 2 && b->chain_mode) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, x) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+                x_map = static_cast<double*>(at.devicePointer);
+            else
+                (void)cudaGetLastError();
+        }
+        bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), (acc || !b->canonical) ? b->hacc.as<double>() : nullptr, s,
+                     x_map);
+        if (!x_map) ck(cudaMemcpyAsync(x, b->hx.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
         if (acc) ck(cudaMemcpyAsync(acc, b->hacc.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
     });
 }

@@ -93,6 +93,15 @@ def test_bound_device_path_matches_host_path(exe):
     bound.sptrsv_host(b, xh)
     torch.cuda.synchronize()
     assert bitwise_equal(xh, host)
+    # pinned (mapped) host buffers: the solve writes x to host memory directly
+    bp = torch.from_numpy(b).pin_memory()
+    xp = torch.full((a.n_rows,), float("nan"), dtype=torch.float64).pin_memory()
+    accp = torch.full((a.n_rows,), float("nan"), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        bound.sptrsv_host(bp.numpy(), xp.numpy(), accp.numpy())
+        torch.cuda.synchronize()
+        assert bitwise_equal(xp.numpy(), host)
+        assert bitwise_equal(accp.numpy(), accd.cpu().numpy())
 
 
 # ---- exec_*_codelet known answers (test_executor.cpp:37-114) ----
