@@ -91,6 +91,17 @@ struct psc_bound {
     bool tiled = false;     // blocks grown over the unit graph (not row ranges)
     bool rec_dirty = true;  // values changed since the records were packed
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
+    // overlapped upload of b (host path, record kernel): copy stream, chunk flags
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_before = nullptr, ev_copied = nullptr;
+    DevBuf b_ready;
+    int* flag_patterns = nullptr;  // pinned, immutable: [i] = 0x01010101 * i (flags are written by the copy engine)
+    ~psc_bound() {
+        if (flag_patterns) cudaFreeHost(flag_patterns);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (ev_before) cudaEventDestroy(ev_before);
+        if (ev_copied) cudaEventDestroy(ev_copied);
+    }
     // general path
     std::vector<int64_t> part_group_ptr;
     DevBuf g_cp, g_fp, g_kind, g_m, g_n, g_form, g_base, g_so, g_si, g_tab, g_tables, g_frow, g_fdiag, g_frhs;
@@ -321,7 +332,8 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     ck(cudaGetLastError(), "spmv launch");
 }
 
-void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s, double* x_host = nullptr) {
+void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s, double* x_host = nullptr,
+                  const int* b_ready = nullptr, int b_shift = 0, int b_flag = 0) {
     use_device(b->device);
     if (b->canonical) {
         if (b->trsv_lean == 2 && b->rec_dirty) {
@@ -337,7 +349,7 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
                       b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
                       b->trsv_lat, b->trsv_lean, b->rec.p, b->unit_len.as<int32_t>(),
                       b->unit_loc.as<int32_t>(), b->halo_ptr.as<int32_t>(), b->halo_col.as<int32_t>(), b->max_block_halo,
-                      b->trsv_lean == 2 ? x_host : nullptr, s);
+                      b->trsv_lean == 2 ? x_host : nullptr, b_ready, b_shift, b_flag, s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");
@@ -470,23 +482,63 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         use_device(b->device);
         const size_t bytes = static_cast<size_t>(b->rows()) * sizeof(double);
-        b->hy.upload_raw(rhs, bytes, s);
+        b->hy.ensure(std::max<size_t>(bytes, 8));
         b->hx.ensure(std::max<size_t>(bytes, 8));
-        if (!b->canonical) b->hx.upload_raw(x, bytes, s);
         if (acc || !b->canonical) b->hacc.ensure(std::max<size_t>(bytes, 8));
         // A pinned, mapped x (UVA) is written by the record kernel directly:
         // every finished chain unit is shipped by one bulk copy, overlapping
-        // the solve instead of a copy after it.
-        double* x_map = nullptr;
-        if (b->canonical && b->trsv_lean == 2 && b->chain_mode) {
+        // the solve instead of a copy after it. A pinned b is then uploaded
+        // in row-ordered chunks on a side stream while the solve runs; the
+        // kernel waits per chunk on arrival flags.
+        auto mapped = [](const void* p) -> const void* {
             cudaPointerAttributes at{};
-            if (cudaPointerGetAttributes(&at, x) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
-                x_map = static_cast<double*>(at.devicePointer);
-            else
-                (void)cudaGetLastError();
+            if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+                return at.devicePointer;
+            (void)cudaGetLastError();
+            return nullptr;
+        };
+        double* x_map = nullptr;
+        if (b->canonical && b->trsv_lean == 2 && b->chain_mode)
+            x_map = static_cast<double*>(const_cast<void*>(mapped(x)));
+        if (x_map && mapped(rhs)) {
+            constexpr int kChunks = 8;
+            int shift = 4;  // chunk rows: a power of two >= 16 (128-byte aligned chunks)
+            while ((static_cast<int64_t>(kChunks) << shift) < b->rows()) ++shift;
+            const int n_chunks = static_cast<int>((b->rows() + (1 << shift) - 1) >> shift);
+            if (!b->copy_stream) {
+                ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&b->ev_before, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&b->ev_copied, cudaEventDisableTiming), "event");
+                b->b_ready.ensure(static_cast<size_t>(n_chunks) * sizeof(int));
+                ck(cudaMemsetAsync(b->b_ready.p, 0, static_cast<size_t>(n_chunks) * sizeof(int), s), "memset");
+                ck(cudaHostAlloc(reinterpret_cast<void**>(&b->flag_patterns), 256 * sizeof(int), cudaHostAllocDefault),
+                   "pinned patterns");
+                for (int i = 0; i < 256; ++i) b->flag_patterns[i] = static_cast<int>(0x01010101u * static_cast<unsigned>(i));
+            }
+            const int next_epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;  // the epoch bound_sptrsv will use
+            const unsigned char pat = static_cast<unsigned char>(next_epoch % 251 + 1);
+            const int flag = static_cast<int>(0x01010101u * pat);
+            ck(cudaEventRecord(b->ev_before, s), "event");  // earlier solves on s are done with hy
+            // the solve goes first (it waits per chunk), then the chunk uploads
+            bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), acc ? b->hacc.as<double>() : nullptr, s, x_map,
+                         b->b_ready.as<int>(), shift, flag);
+            ck(cudaStreamWaitEvent(b->copy_stream, b->ev_before, 0), "wait");
+            for (int c = 0; c < n_chunks; ++c) {
+                const size_t r0 = static_cast<size_t>(c) << shift;
+                const size_t nr = std::min<size_t>(static_cast<size_t>(1) << shift, b->rows() - r0);
+                ck(cudaMemcpyAsync(b->hy.as<double>() + r0, rhs + r0, nr * sizeof(double), cudaMemcpyHostToDevice,
+                                   b->copy_stream), "H2D chunk");
+                ck(cudaMemcpyAsync(b->b_ready.as<int>() + c, b->flag_patterns + pat, sizeof(int), cudaMemcpyHostToDevice,
+                                   b->copy_stream), "flag");
+            }
+            ck(cudaEventRecord(b->ev_copied, b->copy_stream), "event");
+            ck(cudaStreamWaitEvent(s, b->ev_copied, 0), "wait");
+        } else {
+            b->hy.upload_raw(rhs, bytes, s);
+            if (!b->canonical) b->hx.upload_raw(x, bytes, s);
+            bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), (acc || !b->canonical) ? b->hacc.as<double>() : nullptr,
+                         s, x_map);
         }
-        bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), (acc || !b->canonical) ? b->hacc.as<double>() : nullptr, s,
-                     x_map);
         if (!x_map) ck(cudaMemcpyAsync(x, b->hx.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
         if (acc) ck(cudaMemcpyAsync(acc, b->hacc.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
     });

@@ -40,7 +40,7 @@ void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, con
                    int32_t* ticket, int32_t* armed, int epoch, unsigned long long* trace, int threads,
                    int poll_latency, int lean, const void* rec, const int32_t* unit_len,
                    const int32_t* unit_loc, const int32_t* halo_ptr, const int32_t* halo_col, int max_halo,
-                   double* x_host, cudaStream_t stream);
+                   double* x_host, const int* b_ready, int b_shift, int b_flag, cudaStream_t stream);
 size_t trsv_rec_bytes();
 void launch_trsv_pack(const int32_t* ro, const int32_t* col, const double* val, const int32_t* row_block,
                       const int32_t* row_loc, const int32_t* block_row, const int32_t* halo_ptr, const int32_t* halo_key,
