@@ -500,7 +500,16 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
         double* x_map = nullptr;
         if (b->canonical && b->trsv_lean == 2 && b->chain_mode)
             x_map = static_cast<double*>(const_cast<void*>(mapped(x)));
-        if (x_map && mapped(rhs)) {
+        // (not under a profiler: ncu serialises and replays kernels, so a solve
+        // waiting on a concurrent copy would never finish)
+        static const bool overlap = [] {
+            const char* ov = std::getenv("PSC_HOST_OVERLAP");
+            if (ov) return ov[0] != '0';
+            for (const char* v : {"CUDA_INJECTION64_PATH", "NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"})
+                if (std::getenv(v)) return false;  // a profiler (ncu / nsys / sanitizer) is attached
+            return true;
+        }();
+        if (overlap && x_map && mapped(rhs)) {
             constexpr int kChunks = 8;
             int shift = 4;  // chunk rows: a power of two >= 16 (128-byte aligned chunks)
             while ((static_cast<int64_t>(kChunks) << shift) < b->rows()) ++shift;
