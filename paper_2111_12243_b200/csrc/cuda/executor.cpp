@@ -73,6 +73,7 @@ struct psc_bound {
     bool canonical = true, simple = true;
     int n_chunks = 0, n_blocks = 0, max_block_rows = 0, n_sms = 148;
     int64_t n_segments = 0, long_rows = 0;
+    int spmv_short = 0;  // > 0: every row holds <= spmv_short entries (thread-per-row SpMV)
     std::string why_general;
     DevBuf ro, col, val;
     DevBuf rsp, sst, slen, svec, chunk_row, item_seg, long_list, ticket, armed;
@@ -199,6 +200,14 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->long_list.upload(L.long_row_list, s);
             b->n_chunks = static_cast<int>(L.items.size() / 4);
             b->long_rows = L.long_rows;
+            // every row of a simple plan <= 16 entries: thread-per-row kernel (PSC_SPMV_ROWK=0 disables)
+            if (L.simple && L.long_rows == 0) {
+                int32_t mx = 0;
+                for (int32_t r = L.row_begin; r < L.row_end; ++r)
+                    mx = std::max(mx, static_cast<int32_t>(a.row_offsets[r + 1] - a.row_offsets[r]));
+                b->spmv_short = mx <= 16 ? std::max<int32_t>(mx, 1) : 0;
+                if (const char* rk = std::getenv("PSC_SPMV_ROWK"); rk && rk[0] == '0') b->spmv_short = 0;
+            }
             cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
         } else {
             // Solve-round kernel: records (lean 2) for simple rows with <= 4
@@ -324,7 +333,7 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     if (b->canonical) {
         launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
                            b->chunk_row.as<int4>(), b->n_chunks, b->item_seg.as<int2>(), b->long_list.as<int32_t>(),
-                           static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, s);
+                           static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, b->spmv_short, b->rows(), s);
     } else {
         ck(cudaMemsetAsync(y, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset y");
         run_general(b, x, y, nullptr, nullptr, s);

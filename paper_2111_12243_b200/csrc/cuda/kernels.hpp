@@ -25,7 +25,7 @@ struct SegmentsDev {
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                         double* y, const int4* items, int n_items, const int2* item_seg,
                         const int32_t* long_rows, int n_long, SegmentsDev segs, bool accumulate, int n_sms,
-                        cudaStream_t stream);
+                        int short_rows, int n_rows, cudaStream_t stream);
 
 // Sync-free blocked triangular solve (kernels.cu, "blocked sync-free
 // triangular solve"): blocks [block_row[i], block_row[i+1]) of rows, solved by
