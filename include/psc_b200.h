@@ -204,6 +204,39 @@ PSC_API int32_t psc_bound_launches(const psc_bound* b);
  * path (0 parity-segments, 1 general interpreter), algorithmic bytes per call
  * (DESIGN.md), device bytes held, long rows, reserved. */
 PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]);
+/* ---- multi-GPU SpMV: fused x exchange over peer memory --------------------
+ * A rank that bound a shard (psc_bind_partitions) of a simple SpMV plan reads
+ * x entries owned by other ranks. Replaces the reference's none (the
+ * reference is single-node, single-process); DESIGN.md "Multi-GPU". */
+typedef struct psc_peer_window {
+    const double* base;  /* rank q's full-length x window (a peer pointer, or x_window itself) */
+    int32_t row_begin;   /* rows (= x entries) rank q owns: [row_begin, row_end) */
+    int32_t row_end;
+} psc_peer_window;
+
+/* The column runs [runs[2i], runs[2i+1]) outside the shard's own rows that
+ * its multiply reads (runs may be NULL to query the count). */
+PSC_API psc_status psc_bound_x_runs(const psc_bound* b, int32_t* runs, int64_t cap, int64_t* n_runs);
+
+/* y = A_shard x in one launch sequence: the kernel's first CTAs pull the
+ * runs this shard reads from the peers' windows into x_window (which already
+ * holds this rank's own x entries); work that reads only own columns starts
+ * at once, the rest waits for the pulled pieces. Peers must tile the columns
+ * in rank order. The caller orders ranks around it (every window written
+ * before any rank launches; no window rewritten until every rank's launch
+ * finished). Bitwise equal to psc_bound_spmv on the gathered x. */
+PSC_API psc_status psc_bound_spmv_peers(psc_bound* b, const psc_peer_window* peers, int32_t n_peers, double* x_window,
+                                        double* y, void* stream);
+
+/* CUDA IPC helpers for peer windows: allocate shareable device memory and
+ * export its 64-byte handle; open / close a peer's handle; free. */
+PSC_API psc_status psc_ipc_alloc(int64_t bytes, void** ptr, uint8_t handle[64]);
+PSC_API psc_status psc_ipc_open(const uint8_t handle[64], void** ptr);
+PSC_API psc_status psc_ipc_close(void* ptr);
+PSC_API psc_status psc_ipc_free(void* ptr);
+/* Stream-ordered copy between any two (device or host) addresses. */
+PSC_API psc_status psc_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Diagnostic: count mismatches between the solve kernels' division (exact
  * reciprocal refinement + final correction, __ddiv_rn outside exponents
  * [-500, 500]) and IEEE division on n random operand pairs whose exponents

@@ -176,7 +176,20 @@ _SIGS = {
     "psc_int_vector": (None, [c_int64, c_uint64, POINTER(c_double)]),
     "psc_device_count": (c_int32, []),
     "psc_selftest_division": (c_int32, [C.c_uint64, c_int64, c_int32, C.POINTER(c_int64)]),
+    "psc_bound_x_runs": (c_int32, [c_void_p, POINTER(c_int32), c_int64, POINTER(c_int64)]),
+    "psc_bound_spmv_peers": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "psc_ipc_alloc": (c_int32, [c_int64, POINTER(c_void_p), C.c_char_p]),
+    "psc_ipc_open": (c_int32, [C.c_char_p, POINTER(c_void_p)]),
+    "psc_ipc_close": (c_int32, [c_void_p]),
+    "psc_ipc_free": (c_int32, [c_void_p]),
+    "psc_copy_async": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
 }
+
+
+class PeerWindow(Structure):
+    """psc_peer_window (psc_b200.h)."""
+
+    _fields_ = [("base", c_void_p), ("row_begin", c_int32), ("row_end", c_int32)]
 
 _lib = None
 

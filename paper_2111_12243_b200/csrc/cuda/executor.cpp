@@ -74,6 +74,13 @@ struct psc_bound {
     int n_chunks = 0, n_blocks = 0, max_block_rows = 0, n_sms = 148;
     int64_t n_segments = 0, long_rows = 0;
     int spmv_short = 0;  // > 0: every row holds <= spmv_short entries (thread-per-row SpMV)
+    // fused x exchange (sharded simple SpMV): remote column runs and per-work flags
+    bool peer_ok = false;
+    std::vector<int32_t> remote_runs;  // [c0, c1) pairs of columns outside the shard's rows
+    DevBuf remote_block, remote_item, remote_long, peer_pieces, peer_src, peer_ctr;
+    std::vector<int64_t> peer_sig;     // peer table the pieces were built for
+    int n_peer_pieces = 0;
+    unsigned long long peer_done = 0;  // pieces landed so far (device counter mirror)
     std::string why_general;
     DevBuf ro, col, val;
     DevBuf rsp, sst, slen, svec, chunk_row, item_seg, long_list, ticket, armed;
@@ -127,7 +134,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &unit_len, &unit_loc, &row_block, &row_loc, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -207,6 +214,49 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                     mx = std::max(mx, static_cast<int32_t>(a.row_offsets[r + 1] - a.row_offsets[r]));
                 b->spmv_short = mx <= 16 ? std::max<int32_t>(mx, 1) : 0;
                 if (const char* rk = std::getenv("PSC_SPMV_ROWK"); rk && rk[0] == '0') b->spmv_short = 0;
+            }
+            // a shard of a simple plan: the columns it reads outside its own rows
+            // (whose x other ranks own), for the fused exchange
+            if (L.simple && (L.row_begin > 0 || L.row_end < a.n_rows) && a.n_cols == a.n_rows) {
+                std::vector<uint8_t> used(static_cast<size_t>(a.n_cols), 0);
+                auto remote = [&](int32_t c) { return c < L.row_begin || c >= L.row_end; };
+                auto row_remote = [&](int32_t r) {  // local row r
+                    bool any = false;
+                    for (int64_t k = a.row_offsets[r + L.row_begin]; k < a.row_offsets[r + L.row_begin + 1]; ++k) {
+                        const int32_t c = a.col_indices[k];
+                        if (remote(c)) {
+                            used[c] = 1;
+                            any = true;
+                        }
+                    }
+                    return any;
+                };
+                const int32_t nr = b->rows();
+                std::vector<uint8_t> rrow(nr);
+                for (int32_t r = 0; r < nr; ++r) rrow[r] = row_remote(r);
+                std::vector<uint8_t> fb((nr + 255) / 256, 0), fi(L.items.size() / 4, 0), fl(L.long_row_list.size(), 0);
+                for (int32_t r = 0; r < nr; ++r) fb[r / 256] |= rrow[r];
+                for (size_t i = 0; i < fi.size(); ++i)
+                    for (int32_t r = L.items[4 * i]; r < L.items[4 * i + 1]; ++r) fi[i] |= rrow[r];
+                for (size_t i = 0; i < fl.size(); ++i) fl[i] = rrow[L.long_row_list[i]];
+                b->remote_block.upload(fb, s);
+                b->remote_item.upload(fi, s);
+                b->remote_long.upload(fl, s);
+                for (int32_t c = 0; c < a.n_cols;) {  // runs of used columns, gaps < 32 merged
+                    if (!used[c]) {
+                        ++c;
+                        continue;
+                    }
+                    int32_t e = c + 1, last = c;
+                    while (e < a.n_cols && e - last <= 32) {
+                        if (used[e]) last = e;
+                        ++e;
+                    }
+                    b->remote_runs.push_back(c);
+                    b->remote_runs.push_back(last + 1);
+                    c = last + 1;
+                }
+                b->peer_ok = true;
             }
             cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
         } else {
@@ -455,6 +505,118 @@ PSC_API void psc_bound_destroy(psc_bound* b) {
     cudaSetDevice(b->device);
     delete b;
 }
+PSC_API psc_status psc_bound_x_runs(const psc_bound* b, int32_t* runs, int64_t cap, int64_t* n_runs) {
+    return guarded([&] {
+        require(b && n_runs, "x_runs: null argument");
+        require(b->kernel == PSC_KERNEL_SPMV, "x_runs: not an SpMV binding");
+        *n_runs = static_cast<int64_t>(b->remote_runs.size() / 2);
+        if (runs) {
+            require(cap >= *n_runs, "x_runs: buffer too small");
+            std::copy(b->remote_runs.begin(), b->remote_runs.end(), runs);
+        }
+    });
+}
+
+// The fused exchange: see PeerDev (kernels.hpp) and DESIGN.md "Multi-GPU".
+PSC_API psc_status psc_bound_spmv_peers(psc_bound* b, const psc_peer_window* peers, int32_t n_peers, double* x_window,
+                                        double* y, void* stream) {
+    return guarded([&] {
+        require(b && peers && x_window && y && n_peers >= 1, "spmv_peers: null argument");
+        require(b->kernel == PSC_KERNEL_SPMV, "spmv_peers: plan was built for another kernel");
+        require(b->canonical && b->peer_ok, "spmv_peers: needs a shard of a simple (one segment per row) plan");
+        int32_t expect = 0;
+        for (int32_t q = 0; q < n_peers; ++q) {
+            require(peers[q].row_begin == expect && peers[q].row_end >= peers[q].row_begin && peers[q].base,
+                    "spmv_peers: peer windows must tile the rows contiguously");
+            expect = peers[q].row_end;
+        }
+        require(expect == b->n_cols, "spmv_peers: peer windows must cover all columns");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        use_device(b->device);
+        std::vector<int64_t> sig;
+        for (int32_t q = 0; q < n_peers; ++q)
+            sig.insert(sig.end(), {reinterpret_cast<int64_t>(peers[q].base), peers[q].row_begin, peers[q].row_end});
+        sig.push_back(reinterpret_cast<int64_t>(x_window));
+        if (sig != b->peer_sig) {  // pieces {peer, c0, c1}: remote runs split by owner, <= 16384 columns
+            std::vector<int32_t> pc;
+            std::vector<const double*> src(n_peers);
+            for (int32_t q = 0; q < n_peers; ++q) src[q] = peers[q].base;
+            for (size_t i = 0; i + 1 < b->remote_runs.size(); i += 2) {
+                int32_t c = b->remote_runs[i];
+                const int32_t c1 = b->remote_runs[i + 1];
+                int32_t q = 0;
+                while (c < c1) {
+                    while (peers[q].row_end <= c) ++q;
+                    const int32_t e = std::min({c1, peers[q].row_end, c + 16384});
+                    if (peers[q].base != x_window) pc.insert(pc.end(), {q, c, e, 0});
+                    c = e;
+                }
+            }
+            b->n_peer_pieces = static_cast<int>(pc.size() / 4);
+            b->peer_pieces.upload(pc, s);
+            b->peer_src.upload_raw(src.data(), src.size() * sizeof(const double*), s);
+            if (!b->peer_ctr.p) {
+                b->peer_ctr.ensure(2 * sizeof(unsigned long long));
+                ck(cudaMemsetAsync(b->peer_ctr.p, 0, 2 * sizeof(unsigned long long), s), "memset");
+                b->peer_done = 0;
+            }
+            b->peer_sig = sig;
+        }
+        PeerDev P;
+        P.pieces = b->peer_pieces.as<int4>();
+        P.n_pieces = b->n_peer_pieces;
+        P.src = b->peer_src.as<const double*>();
+        P.dst = x_window;
+        P.ticket = b->peer_ctr.as<unsigned long long>();
+        P.done = b->peer_ctr.as<unsigned long long>() + 1;
+        P.ticket_base = 0;
+        b->peer_done += static_cast<unsigned long long>(b->n_peer_pieces);
+        P.done_target = b->peer_done;
+        P.k_pull = std::min(b->n_peer_pieces, 64);
+        P.remote_block = b->remote_block.as<uint8_t>();
+        P.remote_item = b->remote_item.as<uint8_t>();
+        P.remote_long = b->remote_long.as<uint8_t>();
+        ck(cudaMemsetAsync(b->peer_ctr.p, 0, sizeof(unsigned long long), s), "ticket reset");
+        launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x_window, y,
+                           b->chunk_row.as<int4>(), b->n_chunks, b->item_seg.as<int2>(), b->long_list.as<int32_t>(),
+                           static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, b->spmv_short, b->rows(), s, &P);
+        ck(cudaGetLastError(), "spmv_peers launch");
+    });
+}
+
+// Device memory shareable with other processes (CUDA IPC), for peer x windows.
+PSC_API psc_status psc_ipc_alloc(int64_t bytes, void** ptr, uint8_t handle[64]) {
+    return guarded([&] {
+        require(ptr && handle && bytes > 0, "ipc_alloc: bad argument");
+        ck(cudaMalloc(ptr, static_cast<size_t>(bytes)), "ipc_alloc");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, *ptr), "ipc handle");
+        std::memcpy(handle, &h, 64);
+    });
+}
+PSC_API psc_status psc_ipc_open(const uint8_t handle[64], void** ptr) {
+    return guarded([&] {
+        require(ptr && handle, "ipc_open: bad argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, 64);
+        ck(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    });
+}
+PSC_API psc_status psc_ipc_close(void* ptr) {
+    return guarded([&] { ck(cudaIpcCloseMemHandle(ptr), "ipc close"); });
+}
+PSC_API psc_status psc_ipc_free(void* ptr) {
+    return guarded([&] { ck(cudaFree(ptr), "ipc free"); });
+}
+PSC_API psc_status psc_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    return guarded([&] {
+        require(bytes >= 0 && (bytes == 0 || (dst && src)), "copy_async: bad argument");
+        if (bytes)
+            ck(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, static_cast<cudaStream_t>(stream)),
+               "copy_async");
+    });
+}
+
 PSC_API psc_status psc_bound_spmv(psc_bound* b, const double* x, double* y, void* stream) {
     return guarded([&] {
         require(b && x && y, "spmv: null argument");

@@ -17,6 +17,27 @@ struct SegmentsDev {
     const int32_t* seg_vec = nullptr;
 };
 
+// Fused x exchange for multi-GPU SpMV: the first
+// k_pull CTAs of the launch (by ticket, i.e. the first to be scheduled) copy
+// every piece {peer, c0, c1} of x this shard reads from other ranks -- from
+// the peers' x windows over NVLink (src[peer] + c) into the local window dst
+// (the x the kernel gathers from) -- and count them into `done`; work that
+// reads remote columns waits until `done` reaches done_target, everything
+// else proceeds at once. Counters only grow (bases advance per launch).
+struct PeerDev {
+    const int4* pieces = nullptr;           // {peer, c0, c1, 0}
+    int n_pieces = 0;
+    const double* const* src = nullptr;     // device array: peer window base pointers
+    double* dst = nullptr;                  // the local window (== x)
+    unsigned long long* ticket = nullptr;   // CTA tickets (monotonic)
+    unsigned long long* done = nullptr;     // landed pieces (monotonic)
+    unsigned long long ticket_base = 0, done_target = 0;
+    int k_pull = 0;                         // pulling CTAs of this launch (0: nothing to pull)
+    const uint8_t* remote_block = nullptr;  // row kernel: per 256-row block, reads remote columns
+    const uint8_t* remote_item = nullptr;   // chunk kernel: per chunk
+    const uint8_t* remote_long = nullptr;   // long-row kernel: per long row
+};
+
 // y[r] = (accumulate ? y[r] : 0) + sum of row r's segment partials in plan
 // order, each a 4-lane dot (executor.cpp:23-49). items: chunks of short rows
 // {row begin, row end, CSR begin, CSR end} (<= 256 entries and rows each) with
@@ -25,7 +46,8 @@ struct SegmentsDev {
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                         double* y, const int4* items, int n_items, const int2* item_seg,
                         const int32_t* long_rows, int n_long, SegmentsDev segs, bool accumulate, int n_sms,
-                        int short_rows, int n_rows, cudaStream_t stream);
+                        int short_rows, int n_rows, cudaStream_t stream,
+                        const PeerDev* peer = nullptr);
 
 // Sync-free blocked triangular solve (kernels.cu, "blocked sync-free
 // triangular solve"): blocks [block_row[i], block_row[i+1]) of rows, solved by

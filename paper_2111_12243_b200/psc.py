@@ -731,6 +731,26 @@ class BoundPlan:
         _check(_capi.lib().psc_bound_spmv(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
                                           self._stream(stream)))
 
+    def x_runs(self) -> np.ndarray:
+        """Column runs [c0, c1) outside this shard's rows that its multiply reads (shape (n, 2))."""
+        n = C.c_int64()
+        _check(_capi.lib().psc_bound_x_runs(self._h, None, 0, C.byref(n)))
+        out = np.zeros(2 * n.value, dtype=np.int32)
+        _check(_capi.lib().psc_bound_x_runs(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), n.value, C.byref(n)))
+        return out.reshape(-1, 2)
+
+    def spmv_peers(self, peers, x_window, y, stream=None) -> None:
+        """Fused exchange + multiply (psc_bound_spmv_peers): `peers` lists every
+        rank's (window device pointer, row_begin, row_end) in rank order;
+        x_window (this rank's window, a torch CUDA tensor of all columns) holds
+        this rank's own entries."""
+        arr = (_capi.PeerWindow * len(peers))()
+        for i, (ptr, r0, r1) in enumerate(peers):
+            arr[i].base, arr[i].row_begin, arr[i].row_end = int(ptr), int(r0), int(r1)
+        xw = x_window if isinstance(x_window, int) else x_window.data_ptr()
+        _check(_capi.lib().psc_bound_spmv_peers(self._h, C.cast(arr, C.c_void_p), len(peers), C.c_void_p(xw),
+                                                C.c_void_p(y.data_ptr()), self._stream(stream)))
+
     def sptrsv(self, b, x, acc=None, stream=None) -> None:
         _check(_capi.lib().psc_bound_sptrsv(self._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()),
                                             C.c_void_p(acc.data_ptr()) if acc is not None else None,

@@ -186,6 +186,52 @@ def test_partition_shards_bitwise(exe, world):
         assert bitwise_equal(y.cpu().numpy(), want[bound.row_begin:bound.row_end])
 
 
+@pytest.mark.parametrize("config,scale", [(1, 0.25), (5, 0.01), (1, 0.002)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_peer_exchange_bitwise(exe, config, scale, world):
+    """The fused exchange + multiply (psc_bound_spmv_peers): every "rank" has
+    its own x window on this GPU holding only its own entries; each shard's
+    launch pulls the columns it reads from the other windows and multiplies.
+    Stitched shards equal the full plan bitwise, twice in a row (the pull
+    counters advance per launch), and each window ends up holding exactly x
+    on the runs its shard reads. No launch waits on another launch."""
+    import torch
+
+    from paper_2111_12243_b200.dist import shard_partitions
+
+    a = P.generate_config(config, scale)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(a.n_cols, 21)
+    want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+    n_parts = plan.counts().n_partitions
+    bounds, ranges = [], []
+    for r in range(world):
+        p0, p1 = shard_partitions(n_parts, world, r)
+        assert p1 > p0
+        bounds.append(P.BoundPlan(exe, plan, a, partitions=(p0, p1)))
+        ranges.append((bounds[-1].row_begin, bounds[-1].row_end))
+    xt = torch.from_numpy(x).cuda()
+    windows = []
+    for (b, e) in ranges:
+        w = torch.full((a.n_cols,), float("nan"), dtype=torch.float64, device="cuda")
+        w[b:e] = xt[b:e]
+        windows.append(w)
+    peers = [(windows[q].data_ptr(), b, e) for q, (b, e) in enumerate(ranges)]
+    for _ in range(2):
+        ys = []
+        for q, bound in enumerate(bounds):
+            y = torch.full((ranges[q][1] - ranges[q][0],), float("nan"), dtype=torch.float64, device="cuda")
+            bound.spmv_peers(peers, windows[q], y)
+            ys.append(y)
+        torch.cuda.synchronize()
+        got = torch.cat(ys).cpu().numpy()
+        assert bitwise_equal(got, want)
+    for q, bound in enumerate(bounds):
+        w = windows[q].cpu().numpy()
+        for c0, c1 in bound.x_runs():
+            assert bitwise_equal(w[c0:c1], x[c0:c1])
+
+
 def test_general_path_hand_built_plan(exe):
     """A hand-built plan that is not canonical (shared out table, strided gather)
     runs through the exact interpreter and matches the oracle bitwise."""

@@ -80,3 +80,86 @@ def test_two_process_gloo_sharded_spmv():
     assert ok_x, "all-gathered x differs from the original"
     assert ok_y, "stitched shard results differ from the single-process executor"
     assert len(ranges) == 2
+
+
+class _FakeIpc:
+    """Stands in for CUDA IPC: handles name the owner rank's window."""
+
+    calls = []
+
+    @staticmethod
+    def alloc(nbytes):
+        import torch.distributed as dist
+
+        r = dist.get_rank()
+        return 1000 + r, f"h{r}".encode().ljust(64, b"\0")
+
+    @staticmethod
+    def open(handle):
+        return 5000 + int(handle.rstrip(b"\0")[1:])
+
+    @staticmethod
+    def close(ptr):
+        _FakeIpc.calls.append(("close", ptr))
+
+    @staticmethod
+    def free(ptr):
+        _FakeIpc.calls.append(("free", ptr))
+
+    @staticmethod
+    def copy(dst, src, nbytes, stream):
+        _FakeIpc.calls.append(("copy", dst, nbytes))
+
+
+class _FakeBound:
+    def __init__(self):
+        self.calls = []
+
+    def spmv_peers(self, peers, window, y, stream=None):
+        self.calls.append((list(peers), window))
+
+
+def _peer_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_12243_b200.dist import PeerExchange
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ranges = [(0, 7), (7, 10)]
+        bound = _FakeBound()
+        ex = PeerExchange(bound, ranges, rank, 10, ipc=_FakeIpc, device=torch.device("cpu"))
+        x_local = torch.zeros(ranges[rank][1] - ranges[rank][0], dtype=torch.float64)
+        ex.multiply(x_local, torch.zeros(1, dtype=torch.float64), stream=0)
+        ex.close()
+        q.put((rank, ex.peers, bound.calls, _FakeIpc.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_host_protocol():
+    """PeerExchange with fake IPC on 2 gloo processes: every rank's peer table
+    lists its own window and the opened handles of the others in rank order,
+    copies its own slice into its window at the right offset, then launches
+    once with that table; closes what it opened and frees its window."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ranges = [(0, 7), (7, 10)]
+    for rank, peers, calls, ipc_calls in res:
+        want = [((1000 + q) if q == rank else (5000 + q), b, e) for q, (b, e) in enumerate(ranges)]
+        assert peers == want
+        assert calls == [(want, 1000 + rank)]
+        b = ranges[rank][0]
+        assert ipc_calls[0] == ("copy", 1000 + rank + 8 * b, 8 * (ranges[rank][1] - b))
+        other = 1 - rank
+        assert ("close", 5000 + other) in ipc_calls and ("free", 1000 + rank) in ipc_calls
