@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--groups", type=int, default=8)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=6.0, help="bounded CPU-baseline sample length")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                   help="sharded SpMV x exchange: fused peer-memory pull (p2p) or NCCL all-gather")
     return p.parse_args()
 
 
@@ -249,7 +251,35 @@ def run_ours(args):
     out = torch.empty(max(rows, 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
-    if sharded:
+    exchange_kind = None
+    peer_ex = None
+    if sharded and args.exchange == "p2p":
+        # fused exchange: one launch pulls the shard's remote columns from the
+        # peers' IPC windows over NVLink and multiplies (dist.PeerExchange)
+        from paper_2111_12243_b200.dist import PeerExchange, shard_row_ranges
+
+        try:
+            bound.x_runs()  # raises for shards the fused path does not take (segmented plans)
+            peer_ex = PeerExchange(bound, shard_row_ranges(plan, world), rank, a.n_cols)
+        except Exception as e:  # e.g. a segmented plan or no peer access: fall back to NCCL
+            exchange_kind = f"nccl (p2p unavailable: {type(e).__name__}: {e})"
+            peer_ex = None
+        flag = torch.tensor([1 if peer_ex is not None else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if flag.item() == 0 and peer_ex is not None:
+            peer_ex.close()
+            peer_ex = None
+            exchange_kind = exchange_kind or "nccl (p2p unavailable on a peer)"
+    if peer_ex is not None:
+        exchange_kind = "p2p (fused peer-memory pull + multiply)"
+        x_mine = vec[bound.row_begin:bound.row_end].clone()
+
+        def step(ev_mid=None):
+            if ev_mid is not None:
+                ev_mid.record()
+            peer_ex.multiply(x_mine, out)
+    elif sharded:
+        exchange_kind = exchange_kind or "nccl all-gather"
         # every rank owns the x slice of its rows; a step all-gathers x then multiplies
         sizes = torch.tensor([rows], device=dev)
         all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
@@ -389,7 +419,7 @@ def run_ours(args):
         "config": {
             "workload": workload, "kernel": kernel, "n": a.n_rows, "nnz": a.nnz(), "t": args.t,
             "groups": args.groups, "partitions": n_parts, "scale": args.scale,
-            "parallelism": (f"row-sharded x{world} (NCCL all-gather of x)" if sharded else
+            "parallelism": (f"row-sharded x{world} (x exchange: {exchange_kind})" if sharded else
                             (f"replicas x{world}" if world > 1 else "single GPU")),
             "l2": "flushed before every timed step (2x L2 write, outside the events)",
             "mode": "parity (bitwise equal to the reference executor)",

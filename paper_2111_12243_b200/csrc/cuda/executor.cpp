@@ -509,6 +509,7 @@ PSC_API psc_status psc_bound_x_runs(const psc_bound* b, int32_t* runs, int64_t c
     return guarded([&] {
         require(b && n_runs, "x_runs: null argument");
         require(b->kernel == PSC_KERNEL_SPMV, "x_runs: not an SpMV binding");
+        require(b->peer_ok, "x_runs: not a shard of a simple plan (no fused exchange)");
         *n_runs = static_cast<int64_t>(b->remote_runs.size() / 2);
         if (runs) {
             require(cap >= *n_runs, "x_runs: buffer too small");

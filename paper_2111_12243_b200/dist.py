@@ -151,16 +151,22 @@ class PeerExchange:
         if sum(e - b for b, e in ranges) != n_cols or any(
                 b != (ranges[i - 1][1] if i else 0) for i, (b, _) in enumerate(ranges)):
             raise ValueError("PeerExchange: row shards must tile x contiguously")
-        self.window, handle = self.ipc.alloc(8 * max(n_cols, 1))
+        try:
+            self.window, handle = self.ipc.alloc(8 * max(n_cols, 1))
+        except Exception:  # every rank must reach the all-gather; fail together below
+            self.window, handle = 0, None
         handles = [None] * len(ranges)
         dist.all_gather_object(handles, handle, group=group)
         self.opened = {}
+        if any(h is None for h in handles):
+            self.close()
+            raise RuntimeError("PeerExchange: IPC allocation failed on a rank")
         peers = []
         for q, (b, e) in enumerate(ranges):
             if q == rank:
                 ptr = self.window
             else:
-                ptr = self.ipc.open(handles[q])
+                ptr = self.ipc.open(handles[q])  # a failure here is reported to the caller (bench: all-reduced)
                 self.opened[q] = ptr
             peers.append((ptr, b, e))
         self.peers = peers
@@ -169,8 +175,11 @@ class PeerExchange:
         self.token = torch.zeros(1, dtype=torch.float32, device=dev)
 
     def _sync(self):
+        import torch
         import torch.distributed as dist
 
+        if not self.token.is_cuda and torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()  # a host-side collective (gloo) orders nothing on the GPU
         dist.all_reduce(self.token, group=self.group)
 
     def multiply(self, x_local, y, stream=None) -> None:

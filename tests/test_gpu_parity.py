@@ -298,3 +298,67 @@ def test_sptrsv_value_update_repacks(exe):
     second = run_gpu(exe, plan, KernelKind.Sptrsv, a, b)
     assert bitwise_equal(second, run_oracle(plan, KernelKind.Sptrsv, a, b))
     assert not bitwise_equal(first, second)
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_12243_b200.dist import PeerExchange, shard_partitions, shard_row_ranges
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        a = P.generate_config(5, 0.005)
+        plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+        p0, p1 = shard_partitions(plan.counts().n_partitions, world, rank)
+        bound = P.BoundPlan(P.Executor(1, 0), plan, a, partitions=(p0, p1))
+        ranges = shard_row_ranges(plan, world)
+        ex = PeerExchange(bound, ranges, rank, a.n_cols, device=torch.device("cpu"))
+        x = torch.from_numpy(P.uniform_vector(a.n_cols, 31)).cuda()
+        b, e = ranges[rank]
+        outs = []
+        for _ in range(2):
+            y = torch.full((e - b,), float("nan"), dtype=torch.float64, device="cuda")
+            ex.multiply(x[b:e].contiguous(), y)
+            torch.cuda.synchronize()
+            outs.append(y.cpu().numpy())
+        dist.barrier()
+        ex.close()
+        q.put((rank, outs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_real_ipc_two_processes():
+    """Two processes on this GPU exchange real CUDA IPC windows (gloo for the
+    control plane) and multiply their shards through the fused launch; the
+    stitched result equals the oracle bitwise. The processes' kernels never
+    wait on each other (each waits only for its own pulls)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    a = P.generate_config(5, 0.005)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    want = Oracle.run_spmv(plan.export_arrays(), a.view(), P.uniform_vector(a.n_cols, 31))
+    for it in range(2):
+        got = np.concatenate([res[r][it] for r in range(world)])
+        assert bitwise_equal(got, want)
