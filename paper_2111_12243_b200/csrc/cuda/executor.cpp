@@ -269,8 +269,19 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             for (int32_t r = L.row_begin; r < L.row_end; ++r)
                 max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
             const bool lean = L.simple && max_ext <= 4;
-            int want = lean ? 2 : 0;
-            if (const char* ln = std::getenv("PSC_TRSV_LEAN")) want = std::min(want, std::max(0, std::atoi(ln)));
+            // rows the record kernel cannot take: one warp per unit (kernel 3)
+            int want = lean ? 2 : 3;
+            if (const char* ln = std::getenv("PSC_TRSV_LEAN")) {
+                const int v = std::max(0, std::atoi(ln));
+                want = lean ? std::min(want, v) : (v >= 3 ? 3 : std::min(v, 0));
+            }
+            if (want == 3) {  // blocks of ~32 units (two per warp)
+                const int64_t n_units = static_cast<int64_t>(L.unit_start.size());
+                const double avg = n_units ? static_cast<double>(L.row_end - L.row_begin) / static_cast<double>(n_units) : 1.0;
+                int R3 = static_cast<int>(std::min(8192.0, std::max(256.0, 32.0 * avg)));
+                if (const char* env = std::getenv("PSC_SPTRSV_BLOCK_ROWS")) R3 = std::atoi(env);
+                L = lower_plan(p, a, p0, p1, R3, force_general);
+            }
             auto pick_threads = [&](const Lowered& M, int max_halo) {
                 int th = 256;
                 if (M.chain_mode) {  // enough lanes for the units of a block
@@ -288,7 +299,7 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 block_halos(M, a);
                 return M.max_block_rows + M.max_block_halo <= 32767 && pick_threads(M, M.max_block_halo) > 0;
             };
-            b->trsv_lean = lean ? 1 : 0;
+            b->trsv_lean = want == 3 ? 3 : (lean ? 1 : 0);
             if (want == 2) {
                 bool tiles = L.chain_mode;
                 if (const char* tv = std::getenv("PSC_TRSV_TILES")) tiles = tiles && tv[0] != '0';
@@ -308,7 +319,7 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                     }
                 }
             }
-            if (want < b->trsv_lean) b->trsv_lean = want;
+            if (want < b->trsv_lean && want != 3) b->trsv_lean = want;
             b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
             b->chain_mode = L.chain_mode;
             b->tiled = L.tiled;
