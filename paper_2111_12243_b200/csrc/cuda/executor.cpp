@@ -93,6 +93,9 @@ struct psc_bound {
     int trsv_lat = 700;     // cycles before a lane inspects a load it issued (PSC_TRSV_LAT)
     int trsv_lean = 0;      // round kernel for simple rows with <= 4 off-diagonal entries: 1 probed, 2 records
     DevBuf rec;             // trsv_lean == 2: per-row records (trsv_pack_kernel)
+    DevBuf q_units, q_ends, q_next;  // trsv_lean == 4: global unit queue (chain starts / ends)
+    int n_q_units = 0;
+    int q_backoff = 200;  // ns a queue warp sleeps between polls of a missing operand (PSC_TRSV_BACKOFF)
     DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, window slot)
     DevBuf halo_ptr, halo_col, halo_key, halo_pos;  // trsv_lean == 2: per block, the x entries it reads from earlier blocks
     int max_block_halo = -1;
@@ -134,7 +137,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -269,11 +272,50 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             for (int32_t r = L.row_begin; r < L.row_end; ++r)
                 max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
             const bool lean = L.simple && max_ext <= 4;
-            // rows the record kernel cannot take: one warp per unit (kernel 3)
-            int want = lean ? 2 : 3;
+            // rows the record kernel cannot take: a global queue of units, one
+            // warp each (kernel 4); kernel 3 = warp per unit inside row blocks
+            int want = lean ? 2 : 4;
             if (const char* ln = std::getenv("PSC_TRSV_LEAN")) {
                 const int v = std::max(0, std::atoi(ln));
-                want = lean ? std::min(want, v) : (v >= 3 ? 3 : std::min(v, 0));
+                want = lean ? std::min(2, v) : (v >= 3 ? std::min(v, 4) : 0);
+            }
+            if (want == 4) {
+                // units over the whole matrix: chains in row order (chain mode) or
+                // single rows by dependency level (row mode); both topological
+                const int32_t nr = L.row_end - L.row_begin;
+                std::vector<int32_t> lvl(nr, 0);  // dependency level of every row
+                for (int32_t r = 0; r < nr; ++r) {
+                    int32_t m = -1;
+                    for (int32_t k = a.row_offsets[r + L.row_begin]; k < a.row_offsets[r + L.row_begin + 1] - 1; ++k)
+                        m = std::max(m, lvl[a.col_indices[k] - L.row_begin]);
+                    lvl[r] = m + 1;
+                }
+                std::vector<int32_t> units;
+                if (L.chain_mode) {
+                    // chain starts in row order: contiguous chains cannot interleave, so a
+                    // chain depends only on chains that start before it -- the claim order
+                    // is topological (ordering by the first row's level would not be, and
+                    // could exhaust the resident warps on units waiting for unclaimed ones)
+                    for (int32_t r = 0; r < nr; ++r) {
+                        const int32_t gr = r + L.row_begin;
+                        const int32_t k0 = a.row_offsets[gr], kd = a.row_offsets[gr + 1] - 1;
+                        const bool cont = r > 0 && kd > k0 && a.col_indices[kd - 1] == gr - 1;
+                        if (!cont) units.push_back(r);
+                    }
+                    std::vector<int32_t> en(units.size());
+                    for (size_t i = 0; i < units.size(); ++i) en[i] = i + 1 < units.size() ? units[i + 1] : nr;
+                    b->q_ends.upload(en, s);
+                } else {
+                    units.resize(nr);
+                    for (int32_t r = 0; r < nr; ++r) units[r] = r;
+                    std::stable_sort(units.begin(), units.end(), [&](int32_t p, int32_t q) { return lvl[p] < lvl[q]; });
+                }
+                units.push_back(nr);
+                b->q_units.upload(units, s);
+                b->n_q_units = static_cast<int>(units.size()) - 1;
+                b->q_next.ensure(sizeof(int));
+                if (const char* bo = std::getenv("PSC_TRSV_BACKOFF")) b->q_backoff = std::max(0, std::atoi(bo));
+                cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
             }
             if (want == 3) {  // blocks of ~32 units (two per warp)
                 const int64_t n_units = static_cast<int64_t>(L.unit_start.size());
@@ -299,7 +341,7 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 block_halos(M, a);
                 return M.max_block_rows + M.max_block_halo <= 32767 && pick_threads(M, M.max_block_halo) > 0;
             };
-            b->trsv_lean = want == 3 ? 3 : (lean ? 1 : 0);
+            b->trsv_lean = want >= 3 ? want : (lean ? 1 : 0);
             if (want == 2) {
                 bool tiles = L.chain_mode;
                 if (const char* tv = std::getenv("PSC_TRSV_TILES")) tiles = tiles && tv[0] != '0';
@@ -319,7 +361,7 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                     }
                 }
             }
-            if (want < b->trsv_lean && want != 3) b->trsv_lean = want;
+            if (want < b->trsv_lean && want < 3) b->trsv_lean = want;
             b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
             b->chain_mode = L.chain_mode;
             b->tiled = L.tiled;
@@ -405,7 +447,12 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
 void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s, double* x_host = nullptr,
                   const int* b_ready = nullptr, int b_shift = 0, int b_flag = 0) {
     use_device(b->device);
-    if (b->canonical) {
+    if (b->canonical && b->trsv_lean == 4) {
+        launch_sptrsv_queue(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,
+                            b->q_units.as<int32_t>(), b->chain_mode ? b->q_ends.as<int32_t>() : nullptr, b->n_q_units,
+                            !b->chain_mode, b->segs(), b->q_next.as<int>(),
+                            b->trace.as<unsigned long long>(), b->rows(), b->n_sms, b->q_backoff, s);
+    } else if (b->canonical) {
         if (b->trsv_lean == 2 && b->rec_dirty) {
             launch_trsv_pack(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), b->row_block.as<int32_t>(),
                              b->row_loc.as<int32_t>(), b->block_row.as<int32_t>(), b->halo_ptr.as<int32_t>(),

@@ -63,6 +63,12 @@ void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, con
                    int poll_latency, int lean, const void* rec, const int32_t* unit_len,
                    const int32_t* unit_loc, const int32_t* halo_ptr, const int32_t* halo_col, int max_halo,
                    double* x_host, const int* b_ready, int b_shift, int b_flag, cudaStream_t stream);
+// Global unit queue solve (long rows): units = first rows of the chains
+// (units[n_units] = n_rows) or single rows, in topological order.
+void launch_sptrsv_queue(const int32_t* ro, const int32_t* col, const double* val, const double* b, double* x,
+                         double* acc_out, const int32_t* units, const int32_t* unit_end, int n_units,
+                         bool single_row_units, SegmentsDev s, int* next_unit, unsigned long long* trace, int n_rows,
+                         int n_sms, int backoff_ns, cudaStream_t stream);
 size_t trsv_rec_bytes();
 void launch_trsv_pack(const int32_t* ro, const int32_t* col, const double* val, const int32_t* row_block,
                       const int32_t* row_loc, const int32_t* block_row, const int32_t* halo_ptr, const int32_t* halo_key,

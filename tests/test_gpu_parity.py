@@ -266,7 +266,7 @@ def test_division_matches_ieee():
         assert bad.value == 0, (span, bad.value)
 
 
-@pytest.mark.parametrize("lean", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("lean", ["0", "1", "2", "3", "4"])
 @pytest.mark.parametrize("block_rows", ["1024", "0"])
 def test_sptrsv_round_kernels_bitwise(monkeypatch, lean, block_rows):
     """Every solve-round kernel (generic, probed, record-driven), with default
