@@ -41,3 +41,15 @@ timeit("D2H 8 B/row (pinned)", lambda: xh.copy_(xd, non_blocking=True))
 timeit("solve, device buffers", lambda: bound.sptrsv(bd, xd))
 timeit("host path, pinned b and x (overlapped)", lambda: bound.sptrsv_host(bh.numpy(), xh.numpy()))
 timeit("host path, pinned b, pageable x", lambda: bound.sptrsv_host(bh.numpy(), xpage))
+
+import time  # noqa: E402
+
+for label, fn in (("host path, pinned b and x (overlapped)", lambda: bound.sptrsv_host(bh.numpy(), xh.numpy())),):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(20):
+        fn()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"{label}: host enqueue {(t1 - t0) / 20 * 1e6:.1f} us/call, wall {(t2 - t0) / 20 * 1e6:.1f} us/call")
