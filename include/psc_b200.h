@@ -158,6 +158,13 @@ PSC_API psc_status psc_plan_partition_rows(const psc_plan* plan, int64_t part_be
 PSC_API psc_status psc_validate_plan(const psc_plan* plan, const psc_csr_view* a);
 PSC_API void psc_plan_destroy(psc_plan* plan);
 
+/* Binary plan files (the reference only writes a JSON dump,
+ * plan_io.cpp:52-83): the plan as held in memory, reloadable without
+ * re-inspection. Validate a loaded plan against its matrix with
+ * psc_validate_plan before executing it. */
+PSC_API psc_status psc_plan_save(const psc_plan* plan, const char* path);
+PSC_API psc_status psc_plan_load(const char* path, psc_plan** out);
+
 /* ---- executor (executor.hpp:36-51) -----------------------------------------
  * workers < 1 -> PSC_ERR_INVALID_ARGUMENT (executor.cpp:253-255). The worker
  * count is accepted for API compatibility; the GPU schedule never depends on

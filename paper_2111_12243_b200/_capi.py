@@ -183,6 +183,8 @@ _SIGS = {
     "psc_ipc_close": (c_int32, [c_void_p]),
     "psc_ipc_free": (c_int32, [c_void_p]),
     "psc_copy_async": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "psc_plan_save": (c_int32, [c_void_p, c_char_p]),
+    "psc_plan_load": (c_int32, [c_char_p, POINTER(c_void_p)]),
 }
 
 

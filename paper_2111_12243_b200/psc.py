@@ -447,6 +447,21 @@ class CodeletPlan:
         _check(_capi.lib().psc_plan_hash(self._h, self._view(), C.byref(out)))
         return out.value
 
+    def save(self, path: str) -> None:
+        """Write the plan to a binary plan file (psc_plan_save)."""
+        _check(_capi.lib().psc_plan_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load(path: str, matrix: Optional[CsrMatrix] = None) -> "CodeletPlan":
+        """Read a binary plan file (psc_plan_load). Mined plans need the matrix
+        they were mined from to materialise their tables; it is validated."""
+        h = C.c_void_p()
+        _check(_capi.lib().psc_plan_load(str(path).encode(), C.byref(h)))
+        plan = CodeletPlan(h, matrix)
+        if matrix is not None:
+            validate_plan(plan, matrix)
+        return plan
+
     def totals(self):
         cost, ops = C.c_int64(), C.c_int64()
         by = (C.c_int64 * 3)()
@@ -462,7 +477,9 @@ class CodeletPlan:
     @property
     def partitions(self) -> List[PartitionPlan]:
         if self._partitions is None:
-            self._partitions = _arrays_to_partitions(*self.export_arrays()[:2], self._counts)
+            counts, arrays, keep = self.export_arrays()  # `keep` owns the buffers `arrays` points into
+            self._partitions = _arrays_to_partitions(counts, arrays, self._counts)
+            del keep
         return self._partitions
 
     @staticmethod

@@ -188,3 +188,35 @@ def test_inspector_threads_do_not_change_the_plan():
     a = P.generate_config(5, 0.002)
     assert P.inspect(KernelKind.Spmv, a, 3, 8, threads=1).hash() == P.inspect(KernelKind.Spmv, a, 3, 8,
                                                                                threads=8).hash()
+
+
+def test_plan_file_round_trip(tmp_path):
+    """Binary plan files (psc_plan_save / psc_plan_load):
+    mined and imported plans reload with the same digest and arrays; a
+    damaged file is rejected."""
+    import numpy as np
+
+    for kernel, a in ((P.KernelKind.Spmv, P.generate_config(1, 0.003)),
+                      (P.KernelKind.Sptrsv, P.generate_config(2, 0.02))):
+        plan = P.inspect(kernel, a, 3, 8)
+        path = tmp_path / f"plan_{int(kernel)}.bin"
+        plan.save(path)
+        back = P.CodeletPlan.load(path, a)
+        assert back.hash() == plan.hash()
+        c0, arr0, _ = plan.export_arrays()
+        c1, arr1, _ = back.export_arrays()
+        assert (c0.n_groups, c0.n_codelets, c0.n_table) == (c1.n_groups, c1.n_codelets, c1.n_table)
+        imported = P.CodeletPlan.from_partitions(plan.kernel, plan.n_rows, plan.n_cols, plan.nnz, plan.window,
+                                                 plan.target_groups, plan.partitions)
+        ipath = tmp_path / f"imported_{int(kernel)}.bin"
+        imported.save(ipath)
+        assert P.CodeletPlan.load(ipath, a).hash() == plan.hash()
+    bad = tmp_path / "bad.bin"
+    raw = bytearray(path.read_bytes())
+    bad.write_bytes(bytes(raw[: len(raw) // 2]))
+    with pytest.raises(P.InvalidArgument):
+        P.CodeletPlan.load(bad, a)
+    bad.write_bytes(b"not a plan at all")
+    with pytest.raises(P.InvalidArgument):
+        P.CodeletPlan.load(bad)
+    del np
