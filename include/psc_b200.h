@@ -295,6 +295,13 @@ PSC_API void psc_csr_destroy(psc_csr* m);
 PSC_API psc_status psc_csr_from_triplets(int32_t n_rows, int32_t n_cols, int64_t n,
                                          const int32_t* rows, const int32_t* cols,
                                          const double* vals, psc_csr** out);
+/* Matrix Market coordinate files (matrix_market.hpp:24-34): read real,
+ * integer or pattern / general or symmetric (mirrored), duplicates summed,
+ * 0-based; errors are PSC_ERR_INVALID_ARGUMENT "line N: ..." (the reference's
+ * ParseError). Write: coordinate real general, 1-based, 17 significant digits. */
+PSC_API psc_status psc_csr_read_matrix_market(const char* path, psc_csr** out);
+PSC_API psc_status psc_csr_write_matrix_market(const psc_csr_view* a, const char* path);
+
 PSC_API psc_status psc_validate_csr(const psc_csr_view* a);
 PSC_API psc_status psc_lower_triangular(const psc_csr_view* a, psc_csr** out);
 PSC_API psc_status psc_adopt_triangular(const psc_csr_view* a); /* TriangularMatrix::adopt checks */

@@ -195,6 +195,7 @@ class Ref:
             lib.ref_csr_free.argtypes = [c_void_p]
             lib.ref_csr_free.restype = None
             lib.ref_generate_pattern.argtypes = [c_char_p, c_uint64, vp]
+            lib.ref_read_matrix_market.argtypes = [c_char_p, vp, POINTER(C.c_int)]
             lib.ref_csr_from_triplets.argtypes = [c_int, c_int, c_int64, POINTER(C.c_int32), POINTER(C.c_int32),
                                                   POINTER(c_double), vp]
             lib.ref_lower_triangular.argtypes = [c_void_p, vp]
@@ -243,6 +244,15 @@ class Ref:
         h = c_void_p()
         cls._check(cls.lib().ref_csr_from_view(C.byref(view), C.byref(h)))
         return RefCsr(h)
+
+    @classmethod
+    def read_matrix_market(cls, path):
+        """(RefCsr, None) or (None, (parse-error line, message))."""
+        h, line = c_void_p(), C.c_int(0)
+        st = cls.lib().ref_read_matrix_market(str(path).encode(), C.byref(h), C.byref(line))
+        if st != 0:
+            return None, (line.value, cls.lib().ref_last_error().decode())
+        return RefCsr(h), None
 
     @classmethod
     def generate_pattern(cls, spec: str, seed: int = 42) -> RefCsr:

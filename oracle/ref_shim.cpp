@@ -27,6 +27,7 @@
 #include "support/test_helpers.hpp"  // reference tests/support (random_unit_lower, int_vector, ...)
 
 #include "psc_b200.h"
+#include "psc/matrix_market.hpp"
 #include "psc_plan_hash.h"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
@@ -109,6 +110,19 @@ REF_API int ref_csr_view(void* h, psc_csr_view* out) {
     return PSC_OK;
 }
 REF_API void ref_csr_free(void* h) { delete static_cast<RefCsr*>(h); }
+
+// read_matrix_market_file; on a ParseError, *line = its 1-based line
+REF_API int ref_read_matrix_market(const char* path, void** out, int* line) {
+    *line = 0;
+    return guard([&] {
+        try {
+            *out = new RefCsr{psc::read_matrix_market_file(path)};
+        } catch (const psc::ParseError& e) {
+            *line = e.line();
+            throw std::invalid_argument(e.what());
+        }
+    });
+}
 
 REF_API int ref_generate_pattern(const char* spec, uint64_t seed, void** out) {
     return guard([&] { *out = new RefCsr{psc::generate_pattern(spec, seed)}; });

@@ -184,6 +184,8 @@ _SIGS = {
     "psc_ipc_free": (c_int32, [c_void_p]),
     "psc_copy_async": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     "psc_plan_save": (c_int32, [c_void_p, c_char_p]),
+    "psc_csr_read_matrix_market": (c_int32, [c_char_p, POINTER(c_void_p)]),
+    "psc_csr_write_matrix_market": (c_int32, [POINTER(CsrView), c_char_p]),
     "psc_plan_load": (c_int32, [c_char_p, POINTER(c_void_p)]),
 }
 

@@ -155,6 +155,19 @@ class CsrMatrix:
             _capi.lib().psc_csr_destroy(handle)
 
 
+def read_matrix_market(path) -> CsrMatrix:
+    """Matrix Market coordinate file -> CSR (read_matrix_market_file,
+    matrix_market.hpp:24-29); parse errors raise InvalidArgument "line N: ..."."""
+    h = C.c_void_p()
+    _check(_capi.lib().psc_csr_read_matrix_market(str(path).encode(), C.byref(h)))
+    return CsrMatrix._take(h)
+
+
+def write_matrix_market(a: CsrMatrix, path) -> None:
+    """CSR -> coordinate real general, 1-based (write_matrix_market_file)."""
+    _check(_capi.lib().psc_csr_write_matrix_market(C.byref(a.view()), str(path).encode()))
+
+
 @dataclass
 class Triplet:
     row: int = 0
