@@ -295,6 +295,12 @@ PSC_API void psc_csr_destroy(psc_csr* m);
 PSC_API psc_status psc_csr_from_triplets(int32_t n_rows, int32_t n_cols, int64_t n,
                                          const int32_t* rows, const int32_t* cols,
                                          const double* vals, psc_csr** out);
+/* The reference's sequential CSR baselines on host arrays (spmv_csr_baseline /
+ * sptrsv_csr_baseline, executor.cpp:310-340): y = A x, and forward
+ * substitution on a lower triangle with the diagonal stored last. */
+PSC_API psc_status psc_csr_spmv_baseline(const psc_csr_view* a, const double* x, int64_t nx, double* y, int64_t ny);
+PSC_API psc_status psc_csr_sptrsv_baseline(const psc_csr_view* l, const double* b, int64_t nb, double* x, int64_t nx);
+
 /* Matrix Market coordinate files (matrix_market.hpp:24-34): read real,
  * integer or pattern / general or symmetric (mirrored), duplicates summed,
  * 0-based; errors are PSC_ERR_INVALID_ARGUMENT "line N: ..." (the reference's

@@ -185,6 +185,8 @@ _SIGS = {
     "psc_copy_async": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     "psc_plan_save": (c_int32, [c_void_p, c_char_p]),
     "psc_csr_read_matrix_market": (c_int32, [c_char_p, POINTER(c_void_p)]),
+    "psc_csr_spmv_baseline": (c_int32, [POINTER(CsrView), POINTER(c_double), c_int64, POINTER(c_double), c_int64]),
+    "psc_csr_sptrsv_baseline": (c_int32, [POINTER(CsrView), POINTER(c_double), c_int64, POINTER(c_double), c_int64]),
     "psc_csr_write_matrix_market": (c_int32, [POINTER(CsrView), c_char_p]),
     "psc_plan_load": (c_int32, [c_char_p, POINTER(c_void_p)]),
 }

@@ -59,6 +59,33 @@ PSC_API psc_status psc_generate_pattern(const char* spec, uint64_t default_seed,
         *out = new psc_csr{generate_pattern(spec, default_seed)};
     });
 }
+// The reference's sequential baselines (executor.cpp:310-340, SURVEY.md §8a
+// row A13): the NER / verification baselines of the bench report. Plain
+// host loops, built without -march (no FMA contraction).
+PSC_API psc_status psc_csr_spmv_baseline(const psc_csr_view* a, const double* x, int64_t nx, double* y, int64_t ny) {
+    return guarded([&] {
+        require(a && x && y, "spmv_csr_baseline: null argument");
+        require(nx == a->n_cols && ny == a->n_rows, "spmv_csr_baseline: vector size mismatch");
+        for (int32_t i = 0; i < a->n_rows; ++i) {
+            double sum = 0.0;
+            for (int32_t k = a->row_offsets[i]; k < a->row_offsets[i + 1]; ++k) sum += a->values[k] * x[a->col_indices[k]];
+            y[i] = sum;
+        }
+    });
+}
+PSC_API psc_status psc_csr_sptrsv_baseline(const psc_csr_view* l, const double* b, int64_t nb, double* x, int64_t nx) {
+    return guarded([&] {
+        require(l && b && x, "sptrsv_csr_baseline: null argument");
+        require(nb == l->n_rows && nx == l->n_rows, "sptrsv_csr_baseline: vector size mismatch");
+        for (int32_t i = 0; i < l->n_rows; ++i) {
+            double sum = 0.0;
+            const int32_t diag = l->row_offsets[i + 1] - 1;  // diagonal stored last (csr_matrix.hpp:49)
+            for (int32_t k = l->row_offsets[i]; k < diag; ++k) sum += l->values[k] * x[l->col_indices[k]];
+            x[i] = (b[i] - sum) / l->values[diag];
+        }
+    });
+}
+
 PSC_API psc_status psc_generate_config(int32_t config, double scale, uint64_t seed, psc_csr** out) {
     return guarded([&] { *out = new psc_csr{generate_config(config, scale, seed)}; });
 }

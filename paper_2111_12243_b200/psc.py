@@ -155,6 +155,23 @@ class CsrMatrix:
             _capi.lib().psc_csr_destroy(handle)
 
 
+def spmv_csr_baseline(a: CsrMatrix, x: np.ndarray) -> np.ndarray:
+    """The reference's sequential SpMV baseline (executor.cpp:310-323), host."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(a.n_rows)
+    _check(_capi.lib().psc_csr_spmv_baseline(C.byref(a.view()), _dp(x), x.size, _dp(y), y.size))
+    return y
+
+
+def sptrsv_csr_baseline(l, b: np.ndarray) -> np.ndarray:
+    """The reference's forward substitution (executor.cpp:325-340), host."""
+    m = l.csr() if isinstance(l, TriangularMatrix) else l
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty(m.n_rows)
+    _check(_capi.lib().psc_csr_sptrsv_baseline(C.byref(m.view()), _dp(b), b.size, _dp(x), x.size))
+    return x
+
+
 def read_matrix_market(path) -> CsrMatrix:
     """Matrix Market coordinate file -> CSR (read_matrix_market_file,
     matrix_market.hpp:24-29); parse errors raise InvalidArgument "line N: ..."."""
