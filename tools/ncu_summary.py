@@ -20,7 +20,8 @@ KEYS = {
 }
 STALLS = ["long_scoreboard", "wait", "short_scoreboard", "branch_resolving", "barrier", "selected", "no_instructions",
           "lg_throttle", "mio_throttle", "math_pipe_throttle", "membar"]
-UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "msecond": 1e3, "nsecond": 1e-3}
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "msecond": 1e3, "nsecond": 1e-3,
+         "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9, "us": 1, "ms": 1e3, "ns": 1e-3, "s": 1e6, "second": 1e6}
 
 
 def raw(rep):
