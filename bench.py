@@ -157,7 +157,7 @@ def cpu_baseline(kernel, a, plan_t, groups, vec, seconds):
     return {"value": n_flops / med / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": kind,
             "sample": f"{len(times)} complete run_{kernel} calls on the full matrix (median {med * 1e3:.2f} ms), "
                       f"plan t={plan_t} groups={groups}, workers={workers}"
-                      + (" (the reference pool races on deep level-set solves, SURVEY.md §0.8)"
+                      + (" (the reference pool races on deep level-set solves, SURVEY.md §0.8; with 4 or 16 workers it segfaults 3/3 on config 2, tools/ref_workers_probe.py)"
                          if kernel == "sptrsv" and kind == "reference" else ""),
             "ms_median": med * 1e3}
 
