@@ -1,0 +1,112 @@
+"""GPU edge cases for every kernel path, bitwise against the C oracle
+(oracle/psc_oracle.c, pinned to the reference in test_oracle.py): empty and
+tiny matrices, empty rows, rectangular shapes, the boundaries between kernel
+variants (thread-per-row <= 16 entries vs warp chunks; warp chunks <= 256 vs
+long rows; record rounds <= 4 off-diagonal entries vs the unit queue; queue
+rows <= 2048 entries vs its per-lane path), single chains and dense
+triangles."""
+import numpy as np
+import pytest
+
+import paper_2111_12243_b200 as P
+from oracle.oracle import Oracle
+from paper_2111_12243_b200 import KernelKind
+from tests.helpers import bitwise_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(n_rows, n_cols, entries):
+    return P.csr_from_triplets(n_rows, n_cols, entries)
+
+
+def _lower(n, row_cols, seed=0):
+    """Lower triangle: row r has the given off-diagonal columns and a
+    dominant diagonal (stored last)."""
+    rng = np.random.default_rng(seed)
+    ent = []
+    for r in range(n):
+        cs = sorted(set(int(c) for c in row_cols(r) if 0 <= c < r))
+        for c in cs:
+            ent.append((r, c, float(rng.uniform(-1, 1))))
+        ent.append((r, r, float(2 + len(cs) + rng.uniform(0, 1))))
+    return _csr(n, n, ent)
+
+
+def _spmv_check(exe, a, seed=3):
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(a.n_cols, seed)
+    y = np.full(a.n_rows, np.nan)
+    P.run_spmv(plan, a, x, y, exe)
+    assert bitwise_equal(y, Oracle.run_spmv(plan.export_arrays(), a.view(), x))
+
+
+def _sptrsv_check(exe, a, seed=4):
+    plan = P.inspect(KernelKind.Sptrsv, a, 3, 8)
+    b = P.uniform_vector(a.n_rows, seed)
+    x = np.full(a.n_rows, np.nan)
+    acc = np.full(a.n_rows, np.nan)
+    P.run_sptrsv(plan, P.TriangularMatrix.adopt(a), b, x, acc, exe)
+    want, want_acc = Oracle.run_sptrsv(plan.export_arrays(), a.view(), b)[:2]
+    assert bitwise_equal(x, want)
+    assert bitwise_equal(acc, want_acc)
+
+
+def test_spmv_tiny_and_empty(exe):
+    _spmv_check(exe, _csr(1, 1, [(0, 0, 2.5)]))
+    _spmv_check(exe, _csr(5, 3, [(0, 2, 1.0), (4, 0, -2.0)]))  # empty rows, rectangular
+    _spmv_check(exe, _csr(3, 7, [(1, c, 0.5 * c) for c in range(7)]))
+    a = _csr(4, 4, [])
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    y = np.full(4, np.nan)
+    P.run_spmv(plan, a, np.ones(4), y, exe)
+    assert np.array_equal(y, np.zeros(4))
+
+
+@pytest.mark.parametrize("width", [1, 4, 5, 16, 17, 255, 256, 257, 5000])
+def test_spmv_row_length_boundaries(exe, width):
+    """Rows of exactly `width` entries (plus a short row), across the
+    thread-per-row / chunk / long-row boundaries."""
+    n = 300
+    rng = np.random.default_rng(width)
+    ent = []
+    for r in range(n):
+        w = width if r % 3 else 2
+        cols = rng.choice(6000, size=min(w, 6000), replace=False)
+        ent += [(r, int(c), float(rng.uniform(-1, 1))) for c in cols]
+    _spmv_check(exe, _csr(n, 6000, ent))
+
+
+def test_sptrsv_tiny(exe):
+    _sptrsv_check(exe, _csr(1, 1, [(0, 0, 3.0)]))
+    _sptrsv_check(exe, _lower(50, lambda r: []))  # diagonal only
+    _sptrsv_check(exe, _lower(2, lambda r: [r - 1]))
+
+
+def test_sptrsv_single_long_chain(exe):
+    _sptrsv_check(exe, _lower(20000, lambda r: [r - 1]))
+
+
+def test_sptrsv_dense_triangle(exe):
+    """A dense 300 x 300 triangle: rows up to 299 entries (unit queue)."""
+    _sptrsv_check(exe, _lower(300, lambda r: range(r)))
+
+
+def test_sptrsv_row_longer_than_queue_buffer(exe):
+    """One row with 2500 off-diagonal entries (> the queue kernel's
+    2048-entry product buffer: its per-lane path)."""
+    _sptrsv_check(exe, _lower(2600, lambda r: range(r) if r == 2599 else ([r - 1] if r else [])))
+
+
+def test_sptrsv_mixed_short_and_long_rows(exe):
+    """Mostly stencil-like rows with a few wide rows: the plan is not
+    record-eligible as a whole, so the whole solve takes the unit queue."""
+    _sptrsv_check(exe, _lower(3000, lambda r: [r - 1, r - 40, r - 900] if r % 97 else range(max(0, r - 60), r)))
+
+
+@pytest.mark.parametrize("lean", ["0", "1", "2", "4"])
+def test_sptrsv_kernels_on_chain_and_stencil(monkeypatch, lean):
+    monkeypatch.setenv("PSC_TRSV_LEAN", lean)
+    exe = P.Executor(1)
+    _sptrsv_check(exe, _lower(4000, lambda r: [r - 1, r - 63, r - 64 * 64]))
+    _sptrsv_check(exe, _lower(500, lambda r: [r - 2, r - 7]))  # no chains (row mode)
