@@ -433,7 +433,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": total_flops * (1 if sharded else world) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                "path": "psc_bound_*_host (pinned host buffers; SpTRSV: b uploaded in chunks during the solve, x shipped per finished unit by bulk copies)"},
+                "path": "psc_bound_*_host (pinned host buffers; SpTRSV: b gathered from mapped host memory unit by unit in level order during the solve, x shipped per finished unit by bulk copies)"},
         "gpu_launches": args.steps * bound.launches(),
         "clocks": clocks,
         "inspector_seconds": inspector_s,

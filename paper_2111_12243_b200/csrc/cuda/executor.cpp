@@ -105,7 +105,8 @@ struct psc_bound {
     // overlapped upload of b (host path, record kernel): copy stream, chunk flags
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_before = nullptr, ev_copied = nullptr;
-    DevBuf b_ready;
+    DevBuf b_ready, g_order;  // host path: per-unit arrival flags (+ gather ticket), gather order
+    int n_units_total = 0;
     int* flag_patterns = nullptr;  // pinned, immutable: [i] = 0x01010101 * i (flags are written by the copy engine)
     ~psc_bound() {
         if (flag_patterns) cudaFreeHost(flag_patterns);
@@ -137,7 +138,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -371,6 +372,23 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->max_block_units = L.max_block_units;
             b->max_block_halo = -1;
             if (b->trsv_lean == 2) {
+                {   // host path: the order the solve needs b, unit by unit (first rows' dependency levels)
+                    const int32_t nr = b->rows();
+                    std::vector<int32_t> lvl(nr, 0);
+                    for (int32_t r = 0; r < nr; ++r) {
+                        int32_t m = -1;
+                        for (int32_t k = a.row_offsets[r + L.row_begin]; k < a.row_offsets[r + L.row_begin + 1] - 1; ++k)
+                            m = std::max(m, lvl[a.col_indices[k] - L.row_begin]);
+                        lvl[r] = m + 1;
+                    }
+                    std::vector<int32_t> order(L.unit_start.size());
+                    for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
+                    std::stable_sort(order.begin(), order.end(), [&](int32_t p1, int32_t p2) {
+                        return lvl[L.unit_start[p1]] < lvl[L.unit_start[p2]];
+                    });
+                    b->g_order.upload(order, s);
+                    b->n_units_total = static_cast<int>(order.size());
+                }
                 b->unit_len.upload(L.unit_len, s);
                 b->unit_loc.upload(L.unit_loc, s);
                 b->row_block.upload(L.row_block, s);
@@ -705,6 +723,15 @@ PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x, double* y,
         ck(cudaMemcpyAsync(y, b->hy.p, static_cast<size_t>(b->rows()) * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     });
 }
+// CTAs of the unit gather: the SMs the solve leaves free, at least 8 (PSC_GATHER_CTAS overrides)
+static int gather_ctas(int n_sms, int n_blocks) {
+    static const int forced = [] {
+        const char* e = std::getenv("PSC_GATHER_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return forced > 0 ? forced : std::max(8, n_sms - n_blocks);
+}
+
 PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double* x, double* acc, void* stream) {
     return guarded([&] {
         require(b && rhs && x, "sptrsv_host: null argument");
@@ -740,36 +767,31 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
             return true;
         }();
         if (overlap && x_map && mapped(rhs)) {
-            constexpr int kChunks = 8;
-            int shift = 4;  // chunk rows: a power of two >= 16 (128-byte aligned chunks)
-            while ((static_cast<int64_t>(kChunks) << shift) < b->rows()) ++shift;
-            const int n_chunks = static_cast<int>((b->rows() + (1 << shift) - 1) >> shift);
+            // b streams in unit by unit (a gather kernel on a side stream, in the
+            // order the solve needs the units); every solve lane waits for its
+            // unit's rows before staging them
+            const double* rhs_dev = static_cast<const double*>(mapped(rhs));
             if (!b->copy_stream) {
                 ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking), "stream");
                 ck(cudaEventCreateWithFlags(&b->ev_before, cudaEventDisableTiming), "event");
                 ck(cudaEventCreateWithFlags(&b->ev_copied, cudaEventDisableTiming), "event");
-                b->b_ready.ensure(static_cast<size_t>(n_chunks) * sizeof(int));
-                ck(cudaMemsetAsync(b->b_ready.p, 0, static_cast<size_t>(n_chunks) * sizeof(int), s), "memset");
-                ck(cudaHostAlloc(reinterpret_cast<void**>(&b->flag_patterns), 256 * sizeof(int), cudaHostAllocDefault),
-                   "pinned patterns");
-                for (int i = 0; i < 256; ++i) b->flag_patterns[i] = static_cast<int>(0x01010101u * static_cast<unsigned>(i));
+                b->b_ready.ensure(static_cast<size_t>(b->n_units_total + 2) * sizeof(int));
+                ck(cudaMemsetAsync(b->b_ready.p, 0, static_cast<size_t>(b->n_units_total + 2) * sizeof(int), s), "memset");
+                prepare_gather_b_units();
+                cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, b->device);
             }
             const int next_epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;  // the epoch bound_sptrsv will use
-            const unsigned char pat = static_cast<unsigned char>(next_epoch % 251 + 1);
-            const int flag = static_cast<int>(0x01010101u * pat);
+            const int flag = next_epoch % 1000003 + 1;
             ck(cudaEventRecord(b->ev_before, s), "event");  // earlier solves on s are done with hy
-            // the solve goes first (it waits per chunk), then the chunk uploads
+            // the solve goes first (its lanes wait per unit), then the gather
             bound_sptrsv(b, b->hy.as<double>(), b->hx.as<double>(), acc ? b->hacc.as<double>() : nullptr, s, x_map,
-                         b->b_ready.as<int>(), shift, flag);
+                         b->b_ready.as<int>(), -1, flag);
             ck(cudaStreamWaitEvent(b->copy_stream, b->ev_before, 0), "wait");
-            for (int c = 0; c < n_chunks; ++c) {
-                const size_t r0 = static_cast<size_t>(c) << shift;
-                const size_t nr = std::min<size_t>(static_cast<size_t>(1) << shift, b->rows() - r0);
-                ck(cudaMemcpyAsync(b->hy.as<double>() + r0, rhs + r0, nr * sizeof(double), cudaMemcpyHostToDevice,
-                                   b->copy_stream), "H2D chunk");
-                ck(cudaMemcpyAsync(b->b_ready.as<int>() + c, b->flag_patterns + pat, sizeof(int), cudaMemcpyHostToDevice,
-                                   b->copy_stream), "flag");
-            }
+            launch_gather_b_units(rhs_dev, b->hy.as<double>(), b->g_order.as<int32_t>(), b->unit_start.as<int32_t>(),
+                                  b->unit_len.as<int32_t>(), b->n_units_total,
+                                  b->b_ready.as<int>() + b->n_units_total, b->b_ready.as<int>(), flag,
+                                  gather_ctas(b->n_sms, b->n_blocks), b->copy_stream);
+            ck(cudaGetLastError(), "gather b");
             ck(cudaEventRecord(b->ev_copied, b->copy_stream), "event");
             ck(cudaStreamWaitEvent(s, b->ev_copied, 0), "wait");
         } else {

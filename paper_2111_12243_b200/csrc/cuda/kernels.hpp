@@ -69,6 +69,13 @@ void launch_sptrsv_queue(const int32_t* ro, const int32_t* col, const double* va
                          double* acc_out, const int32_t* units, const int32_t* unit_end, int n_units,
                          bool single_row_units, SegmentsDev s, int* next_unit, unsigned long long* trace, int n_rows,
                          int n_sms, int backoff_ns, cudaStream_t stream);
+// Host path of the record kernel: b copied from mapped host memory unit by
+// unit in `order`, b_ready[u] = flag when unit u's rows landed (ticket: 2
+// ints, zero before the first launch, self re-arming). Call prepare first.
+void prepare_gather_b_units();
+void launch_gather_b_units(const double* b_host, double* b_dev, const int32_t* order, const int32_t* unit_start,
+                           const int32_t* unit_len, int n_units, int* ticket, int* b_ready, int flag, int n_ctas,
+                           cudaStream_t stream);
 size_t trsv_rec_bytes();
 void launch_trsv_pack(const int32_t* ro, const int32_t* col, const double* val, const int32_t* row_block,
                       const int32_t* row_loc, const int32_t* block_row, const int32_t* halo_ptr, const int32_t* halo_key,
