@@ -60,3 +60,11 @@ blk = np.arange(n) // info["max_block_rows"]
 for k in list(range(0, nb, max(1, nb // 8)))[:10]:
     m = blk == k
     print(f"block {k}: rows finish {t_rows[m].min()/1e3:.1f}..{t_rows[m].max()/1e3:.1f} us, levels {level[m].min()}..{level[m].max()}")
+if cfg == 2 and scale == 1.0:  # per-line cadence inside the first planes (rows r = x + 100 y + 10000 z)
+    N = 100
+    for z in (0, 1, 50):
+        t = t_rows[z * N * N:(z + 1) * N * N].reshape(N, N)  # [y][x]
+        first = t[:, 0] / 1e3
+        step_x = np.median(np.diff(t, axis=1), axis=1)  # per line: median time between consecutive rows
+        print(f"plane z={z}: line start (us) y=0,1,2,31,32,63,64,99: {[round(first[i], 2) for i in (0, 1, 2, 31, 32, 63, 64, 99)]}")
+        print(f"  median row step along x (ns) y=0,1,31,32,99: {[int(step_x[i]) for i in (0, 1, 31, 32, 99)]}; line end (us) y=0,99: {round(t[0,-1]/1e3,2)}, {round(t[99,-1]/1e3,2)}")
