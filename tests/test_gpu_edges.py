@@ -110,3 +110,45 @@ def test_sptrsv_kernels_on_chain_and_stencil(monkeypatch, lean):
     exe = P.Executor(1)
     _sptrsv_check(exe, _lower(4000, lambda r: [r - 1, r - 63, r - 64 * 64]))
     _sptrsv_check(exe, _lower(500, lambda r: [r - 2, r - 7]))  # no chains (row mode)
+
+
+@pytest.mark.parametrize("with_acc", [True, False])
+def test_sptrsv_division_fallback(exe, with_acc):
+    """Diagonals and right-hand sides far outside the exponent range of the
+    reciprocal-based division ([-500, 500]): the record kernel's rare
+    __ddiv_rn fallback (for t = b - acc and for the diagonal, flagged at pack
+    time), with and without the acc output (separate kernel instantiations),
+    bitwise against the oracle."""
+    import torch
+
+    n = 3000
+    rng = np.random.default_rng(11)
+    ent = []
+    for r in range(n):
+        cs = [c for c in (r - 1, r - 40, r - 900) if c >= 0]
+        for c in cs:
+            ent.append((r, c, float(rng.uniform(-1, 1))))
+        d = 2.0 + len(cs)
+        if r % 7 == 3:
+            d *= 1e-160  # tiny diagonal: flagged at pack time
+        elif r % 11 == 5:
+            d *= 1e170  # huge diagonal
+        ent.append((r, r, d))
+    a = _csr(n, n, ent)
+    plan = P.inspect(KernelKind.Sptrsv, a, 3, 8)
+    b = P.uniform_vector(n, 12)
+    b[::13] *= 1e-300  # tiny and subnormal-range right-hand sides
+    b[5::17] *= 1e200
+    want, want_acc = Oracle.run_sptrsv(plan.export_arrays(), a.view(), b)[:2]
+    bound = P.BoundPlan(exe, plan, a)
+    bd = torch.from_numpy(b).cuda()
+    xd = torch.full_like(bd, float("nan"))
+    if with_acc:
+        accd = torch.full_like(bd, float("nan"))
+        bound.sptrsv(bd, xd, accd)
+    else:
+        bound.sptrsv(bd, xd)
+    torch.cuda.synchronize()
+    assert bitwise_equal(xd.cpu().numpy(), want)
+    if with_acc:
+        assert bitwise_equal(accd.cpu().numpy(), want_acc)
