@@ -96,6 +96,9 @@ struct psc_bound {
     DevBuf q_units, q_ends, q_next;  // trsv_lean == 4: global unit queue (chain starts / ends)
     int n_q_units = 0;
     int q_backoff = 200;  // ns a queue warp sleeps between polls of a missing operand (PSC_TRSV_BACKOFF)
+    DevBuf s_pieces;      // trsv_lean == 4, chain mode: <= 32-row pieces of the chain units (streaming kernel)
+    int n_s_pieces = 0;   // 0: the warp-per-row queue kernel
+    int stream_k = 8;     // entries a lane consumes per round (PSC_TRSV_STREAM_K)
     DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, window slot)
     DevBuf halo_ptr, halo_col, halo_key, halo_pos;  // trsv_lean == 2: per block, the x entries it reads from earlier blocks
     int max_block_halo = -1;
@@ -138,7 +141,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -306,6 +309,17 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                     std::vector<int32_t> en(units.size());
                     for (size_t i = 0; i < units.size(); ++i) en[i] = i + 1 < units.size() ? units[i + 1] : nr;
                     b->q_ends.upload(en, s);
+                    // streaming kernel (lane per row): the chains cut into pieces of <= 32 rows
+                    const char* sv = std::getenv("PSC_TRSV_STREAM");
+                    if (!(sv && sv[0] == '0')) {
+                        std::vector<int32_t> pieces;
+                        for (size_t i = 0; i < units.size(); ++i)
+                            for (int32_t r = units[i]; r < en[i]; r += 32) pieces.push_back(r);
+                        pieces.push_back(nr);
+                        b->s_pieces.upload(pieces, s);
+                        b->n_s_pieces = static_cast<int>(pieces.size()) - 1;
+                        if (const char* k = std::getenv("PSC_TRSV_STREAM_K")) b->stream_k = std::atoi(k);
+                    }
                 } else {
                     units.resize(nr);
                     for (int32_t r = 0; r < nr; ++r) units[r] = r;
@@ -465,7 +479,11 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
 void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaStream_t s, double* x_host = nullptr,
                   const int* b_ready = nullptr, int b_shift = 0, int b_flag = 0) {
     use_device(b->device);
-    if (b->canonical && b->trsv_lean == 4) {
+    if (b->canonical && b->trsv_lean == 4 && b->n_s_pieces > 0) {
+        launch_sptrsv_stream(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,
+                             b->s_pieces.as<int32_t>(), b->n_s_pieces, b->segs(), b->q_next.as<int>(),
+                             b->trace.as<unsigned long long>(), b->rows(), b->n_sms, b->stream_k, s);
+    } else if (b->canonical && b->trsv_lean == 4) {
         launch_sptrsv_queue(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,
                             b->q_units.as<int32_t>(), b->chain_mode ? b->q_ends.as<int32_t>() : nullptr, b->n_q_units,
                             !b->chain_mode, b->segs(), b->q_next.as<int>(),
