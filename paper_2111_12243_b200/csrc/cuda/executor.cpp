@@ -98,7 +98,7 @@ struct psc_bound {
     int q_backoff = 200;  // ns a queue warp sleeps between polls of a missing operand (PSC_TRSV_BACKOFF)
     DevBuf s_pieces;      // trsv_lean == 4, chain mode: <= 32-row pieces of the chain units (streaming kernel)
     int n_s_pieces = 0;   // 0: the warp-per-row queue kernel
-    int stream_k = 8;     // entries a lane consumes per round (PSC_TRSV_STREAM_K)
+    int stream_k = 8;     // entries a lane consumes per round
     DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, window slot)
     DevBuf halo_ptr, halo_col, halo_key, halo_pos;  // trsv_lean == 2: per block, the x entries it reads from earlier blocks
     int max_block_halo = -1;
@@ -318,7 +318,6 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                         pieces.push_back(nr);
                         b->s_pieces.upload(pieces, s);
                         b->n_s_pieces = static_cast<int>(pieces.size()) - 1;
-                        if (const char* k = std::getenv("PSC_TRSV_STREAM_K")) b->stream_k = std::atoi(k);
                     }
                 } else {
                     units.resize(nr);

@@ -58,3 +58,36 @@ for lo, hi in ((0, 64), (64, 128), (128, 256), (256, 512), (512, 10 ** 9)):
     if sel.any():
         print(f"  in-chain rows with {lo}-{hi} entries: {sel.sum()} rows, median {np.median(gap[sel]):.0f} ns")
 print(f"row length: median {np.median(ln):.0f}, p99 {np.percentile(ln, 99):.0f}, max {ln.max()}")
+# streaming kernel pieces: chain units cut every 32 rows
+piece = np.zeros(n, dtype=np.int64)
+pid, start = -1, 0
+for r in range(n):
+    k0, kd = ro[r], ro[r + 1] - 1
+    cont = r > 0 and kd > k0 and col[kd - 1] == r - 1
+    if not cont or r - start >= 32:
+        pid += 1
+        start = r if not cont or r - start >= 32 else start
+        if not cont:
+            start = r
+    piece[r] = pid
+same = has & (piece[np.maximum(last_dep, 0)] == piece)
+print(f"latest operand in the same piece: {same.mean():.2%} (median gap {np.median(gap[same]):.0f} ns); "
+      f"in another piece: {(has & ~same).mean():.2%} (median gap {np.median(gap[has & ~same]):.0f} ns)")
+r = int(np.argmax(t))
+hops_same = hops_other = 0
+t_same = t_other = 0
+while last_dep[r] >= 0:
+    d = int(last_dep[r])
+    if piece[d] == piece[r]:
+        hops_same += 1
+        t_same += t[r] - t[d]
+    else:
+        hops_other += 1
+        t_other += t[r] - t[d]
+    r = d
+print(f"critical path: {hops_same} in-piece hops ({t_same / 1e6:.2f} ms, {t_same / max(hops_same, 1):.0f} ns each), "
+      f"{hops_other} cross-piece hops ({t_other / 1e6:.2f} ms, {t_other / max(hops_other, 1):.0f} ns each)")
+st4 = buf[n:n + 4].astype(np.float64)  # streaming kernel: rounds with / without L2 operand loads, and their cycles
+if st4[0] + st4[2] > 0:
+    print(f"stream rounds (2 solves, all warps): with L2 loads {st4[0]:.0f} ({st4[1] / max(st4[0], 1):.0f} cycles each), "
+          f"smem only {st4[2]:.0f} ({st4[3] / max(st4[2], 1):.0f} cycles each)")
