@@ -2,5 +2,5 @@
 timeout 900 python -m pytest tests -m gpu -q -x -k "sptrsv or trsv or edge or configs" > gpurun_out/st_pytest.log 2>&1; tail -1 gpurun_out/st_pytest.log
 b() { timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/st.json 2>&1; python -c "
 import json; d=json.loads(open('gpurun_out/st.json').read().strip().splitlines()[-1]); print('$1', d['parity'], 'kernel ms', round(d['roofline']['kernel_ms'],3), 'GF', round(d['value'],2))" || tail -5 gpurun_out/st.json; }
-for w in 4 8; do for p in 0 1; do PSC_TRSV_BACKOFF=$p PSC_TRSV_STREAM_WARPS=$w b "warps$w poll1=$p"; done; done
-PSC_TRSV_BACKOFF=0 PSC_TRSV_STREAM_WARPS=4 timeout 600 python tools/trace_c4.py | tail -3
+for w in 4 8; do PSC_TRSV_STREAM_WARPS=$w b "warps$w"; done
+timeout 600 python tools/trace_c4.py | tail -3
