@@ -92,16 +92,31 @@ def test_sptrsv_dense_triangle(exe):
     _sptrsv_check(exe, _lower(300, lambda r: range(r)))
 
 
-def test_sptrsv_row_longer_than_queue_buffer(exe):
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_sptrsv_row_longer_than_queue_buffer(monkeypatch, stream):
     """One row with 2500 off-diagonal entries (> the queue kernel's
-    2048-entry product buffer: its per-lane path)."""
+    2048-entry product buffer: its per-lane path; > the streaming kernel's
+    staged row tail)."""
+    monkeypatch.setenv("PSC_TRSV_STREAM", stream)
+    exe = P.Executor(1)
     _sptrsv_check(exe, _lower(2600, lambda r: range(r) if r == 2599 else ([r - 1] if r else [])))
 
 
-def test_sptrsv_mixed_short_and_long_rows(exe):
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_sptrsv_mixed_short_and_long_rows(monkeypatch, stream):
     """Mostly stencil-like rows with a few wide rows: the plan is not
-    record-eligible as a whole, so the whole solve takes the unit queue."""
+    record-eligible as a whole, so the whole solve takes the long-row path:
+    the lane-per-row streaming kernel (chain mode) or the warp-per-row unit
+    queue (PSC_TRSV_STREAM=0)."""
+    monkeypatch.setenv("PSC_TRSV_STREAM", stream)
+    exe = P.Executor(1)
     _sptrsv_check(exe, _lower(3000, lambda r: [r - 1, r - 40, r - 900] if r % 97 else range(max(0, r - 60), r)))
+    # supernode-like dense triangles longer than a 32-row piece, with dense runs over earlier ones
+    def rows(r):
+        s0 = (r // 45) * 45
+        prev = list(range(max(0, s0 - 45), s0)) if r % 3 else []
+        return prev + list(range(s0, r))
+    _sptrsv_check(exe, _lower(1000, rows))
 
 
 @pytest.mark.parametrize("lean", ["0", "1", "2", "4"])
