@@ -84,6 +84,8 @@ struct psc_bound {
     std::string why_general;
     DevBuf ro, col, val;
     DevBuf rsp, sst, slen, svec, chunk_row, item_seg, long_list, ticket, armed;
+    DevBuf groups;      // SpMV row groups {r0, g} (segmented plans)
+    int n_groups = 0;
     bool chain_mode = false;
     int max_block_units = 0;
     DevBuf block_row, block_unit, unit_start;
@@ -126,7 +128,7 @@ struct psc_bound {
     int32_t rows() const { return row_end - row_begin; }
     SegmentsDev segs() const {
         if (simple) return {};
-        return {rsp.as<int32_t>(), sst.as<int32_t>(), slen.as<int32_t>(), svec.as<int32_t>()};
+        return {rsp.as<int32_t>(), sst.as<int32_t>(), slen.as<int32_t>(), svec.as<int32_t>(), groups.as<int4>(), n_groups};
     }
     GeneralDev gen() const {
         return {g_cp.as<int64_t>(),  g_fp.as<int64_t>(),  g_kind.as<int32_t>(), g_m.as<int32_t>(),
@@ -141,7 +143,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -213,6 +215,8 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->item_seg.upload(L.item_seg, s);
             b->long_list.upload(L.long_row_list, s);
             b->n_chunks = static_cast<int>(L.items.size() / 4);
+            b->groups.upload(L.groups, s);
+            b->n_groups = static_cast<int>(L.groups.size() / 8);
             b->long_rows = L.long_rows;
             // every row of a simple plan <= 16 entries: thread-per-row kernel (PSC_SPMV_ROWK=0 disables)
             if (L.simple && L.long_rows == 0) {
@@ -834,7 +838,11 @@ PSC_API int64_t psc_bound_trace(const psc_bound* b, uint64_t* out, int64_t cap) 
 }
 PSC_API int32_t psc_bound_launches(const psc_bound* b) {
     if (!b) return 0;
-    if (b->canonical) return b->kernel == PSC_KERNEL_SPMV && b->long_rows > 0 && b->n_chunks > 0 ? 2 : 1;
+    if (b->canonical) {
+        if (b->kernel != PSC_KERNEL_SPMV) return 1;
+        const int n = (b->long_rows > 0) + (b->n_chunks > 0) + (b->n_groups > 0);
+        return n > 0 ? n : 1;
+    }
     return static_cast<int32_t>(b->part_group_ptr.size()) - 1;
 }
 PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]) {

@@ -15,6 +15,8 @@ struct SegmentsDev {
     const int32_t* seg_start = nullptr;
     const int32_t* seg_len = nullptr;
     const int32_t* seg_vec = nullptr;
+    const int4* groups = nullptr;  // SpMV row groups, 2 int4 each (lower.hpp Lowered::groups)
+    int n_groups = 0;
 };
 
 // Fused x exchange for multi-GPU SpMV: the first

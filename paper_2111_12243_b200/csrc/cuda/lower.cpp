@@ -340,6 +340,42 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
     if (p.kernel == PSC_KERNEL_SPMV) {
         auto k_of = [&](int32_t r) { return static_cast<int32_t>(ro[r + L.row_begin] - L.k_begin); };
         auto s_of = [&](int32_t r) { return L.simple ? 0 : L.row_seg_ptr[r]; };
+        // row groups (segmented plans): rows whose segments are unit-stride
+        // gathers tiling the row in CSR order, consecutive rows with the same
+        // lengths and x offsets
+        std::vector<int32_t> group_len(nr, 0);  // > 0 at a group's first row
+        const char* gv = std::getenv("PSC_SPMV_GROUPS");
+        if (!L.simple && !(gv && gv[0] == '0')) {
+            auto templ = [&](int32_t r) {  // row r qualifies as a template
+                const int32_t q0 = L.row_seg_ptr[r], q1 = L.row_seg_ptr[r + 1];
+                const int32_t len = k_of(r + 1) - k_of(r);
+                if (q1 - q0 < 1 || q1 - q0 > 32 || len < 1 || len > kGroupCols) return false;
+                int32_t at = k_of(r);
+                for (int32_t q = q0; q < q1; ++q) {
+                    if (L.seg_vec[q] < 0 || L.seg_start[q] != at) return false;
+                    at += L.seg_len[q];
+                }
+                return at == k_of(r + 1);
+            };
+            auto same = [&](int32_t r, int32_t t) {  // row t has row r's template
+                const int32_t q0 = L.row_seg_ptr[r], q1 = L.row_seg_ptr[r + 1], d = L.row_seg_ptr[t] - q0;
+                if (L.row_seg_ptr[t + 1] - L.row_seg_ptr[t] != q1 - q0) return false;
+                for (int32_t q = q0; q < q1; ++q)
+                    if (L.seg_len[q + d] != L.seg_len[q] || L.seg_vec[q + d] != L.seg_vec[q]) return false;
+                return true;
+            };
+            for (int32_t r = 0; r < nr;) {
+                int32_t g = 1;
+                if (templ(r))
+                    while (g < kGroupRows && r + g < nr && templ(r + g) && same(r, r + g)) ++g;
+                if (g >= 2) {
+                    group_len[r] = g;
+                    const int32_t q0 = L.row_seg_ptr[r];
+                    L.groups.insert(L.groups.end(), {r, g, k_of(r), k_of(r + 1) - k_of(r), q0, L.row_seg_ptr[r + 1] - q0, 0, 0});
+                }
+                r += g;
+            }
+        }
         int32_t c0 = 0;  // start of the open chunk
         auto close = [&](int32_t r1) {
             if (r1 > c0) {
@@ -348,6 +384,12 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
             }
         };
         for (int32_t r = 0; r < nr; ++r) {
+            if (group_len[r] > 0) {  // a row group: not in any chunk
+                close(r);
+                r += group_len[r] - 1;
+                c0 = r + 1;
+                continue;
+            }
             const int64_t len = ro[r + L.row_begin + 1] - ro[r + L.row_begin];
             if (len > kSpmvWarpCap) {  // a long row is handled on its own
                 close(r);

@@ -43,6 +43,14 @@ struct Lowered {
     std::vector<int32_t> item_seg;  // 2 per chunk (segmented plans)
     std::vector<int32_t> long_row_list;
     int64_t long_rows = 0;
+    // SpMV row groups (segmented plans): runs of 2..kGroupRows consecutive
+    // rows with the same segment template -- all unit-stride gathers, tiling
+    // the row in CSR order, the same lengths and x offsets -- so the rows read
+    // the same x runs (the dof rows of a block stencil node). {r0, g} each;
+    // their rows are in no chunk. 8 ints per group: {r0, g, k0, C, q0, S, -, -}
+    // (first row, rows, first CSR position, entries per row, first segment,
+    // segments per row).
+    std::vector<int32_t> groups;
     // SpTRSV row blocks in local rows, and every block's rows in
     // dependency-level order (the plan's partition index, then row)
     std::vector<int32_t> block_row;
@@ -80,6 +88,8 @@ struct Lowered {
 };
 
 constexpr int kSpmvWarpCap = 256;  // == kWarpCap in kernels.cu
+constexpr int kGroupRows = 4;      // rows per SpMV row group (== kernels.cu)
+constexpr int kGroupCols = 96;     // entries per row of a row group (three warp passes)
 
 // Lower partitions [part_begin, part_end) (all partitions when part_end < 0).
 // force_general lowers through the exact interpreter even when canonical
