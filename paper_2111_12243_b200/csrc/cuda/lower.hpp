@@ -88,7 +88,7 @@ struct Lowered {
 };
 
 constexpr int kSpmvWarpCap = 256;  // == kWarpCap in kernels.cu
-constexpr int kGroupRows = 4;      // rows per SpMV row group (== kernels.cu)
+constexpr int kGroupRows = 3;      // rows per SpMV row group (== kernels.cu)
 constexpr int kGroupCols = 96;     // entries per row of a row group (three warp passes)
 
 // Lower partitions [part_begin, part_end) (all partitions when part_end < 0).
