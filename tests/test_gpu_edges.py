@@ -167,3 +167,36 @@ def test_sptrsv_division_fallback(exe, with_acc):
     assert bitwise_equal(xd.cpu().numpy(), want)
     if with_acc:
         assert bitwise_equal(accd.cpu().numpy(), want_acc)
+
+
+def _block_rows_matrix(seed=21):
+    """Dense dof blocks over stencil-like neighbour runs: nodes 0..299 with
+    2, 3 or 4 dof (by thirds), neighbours i-1..i+1 and i+-10 (separate x
+    runs); every 50th node reads i-30..i+30 (> 96 entries per row)."""
+    rng = np.random.default_rng(seed)
+    n_nodes = 300
+    dof = np.array([2 if i < 100 else (3 if i < 200 else 4) for i in range(n_nodes)])
+    start = np.concatenate([[0], np.cumsum(dof)])
+    ent = []
+    for i in range(n_nodes):
+        if i % 50 == 7:
+            nbrs = range(max(0, i - 30), min(n_nodes, i + 31))
+        else:
+            nbrs = [j for j in (i - 10, i - 1, i, i + 1, i + 10) if 0 <= j < n_nodes]
+        for d in range(dof[i]):
+            for j in nbrs:
+                for e in range(dof[j]):
+                    ent.append((int(start[i] + d), int(start[j] + e), float(rng.uniform(-1, 1))))
+    n = int(start[-1])
+    return _csr(n, n, ent)
+
+
+@pytest.mark.parametrize("groups", ["1", "0"])
+def test_spmv_row_groups(monkeypatch, groups):
+    """Rows of a node share one BLAS segment template: with groups on they
+    form row groups of 2 or 3 rows (a 4-dof node splits 3 + 1), wide rows
+    and boundary rows stay in chunks. Bitwise against the oracle, with and
+    without groups."""
+    monkeypatch.setenv("PSC_SPMV_GROUPS", groups)
+    exe = P.Executor(1)
+    _spmv_check(exe, _block_rows_matrix())
