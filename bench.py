@@ -237,6 +237,12 @@ def run_ours(args):
     t0 = time.perf_counter()
     plan = P.inspect(kk, a, args.t, args.groups)
     inspector_s = time.perf_counter() - t0
+    # the same inspection with the window mining on the GPU (same plan, bit for bit)
+    t0 = time.perf_counter()
+    plan_dev = P.inspect_device(kk, a, args.t, args.groups, local)
+    inspector_dev_s = time.perf_counter() - t0
+    inspector_dev_same = plan_dev.hash() == plan.hash()
+    del plan_dev
     exe = P.Executor(1, local)
     n_parts = plan.counts().n_partitions
     sharded = kernel == "spmv" and world > 1
@@ -448,6 +454,8 @@ def run_ours(args):
         "gpu_launches": args.steps * bound.launches(),
         "clocks": clocks,
         "inspector_seconds": inspector_s,
+        "inspector_device_seconds": inspector_dev_s,
+        "inspector_device_plan_equal": inspector_dev_same,
     }
     if kernel == "sptrsv":  # the solve is bound by its dependency chain, not by HBM
         line["roofline"]["critical_path"] = {

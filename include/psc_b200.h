@@ -137,6 +137,12 @@ typedef struct psc_exec_context psc_exec_context; /* ExecutionContext, defined b
  * threads <= 0 uses every hardware thread; the plan never depends on it. */
 PSC_API psc_status psc_inspect(int32_t kernel, const psc_csr_view* a, int32_t t,
                                int32_t target_groups, int32_t threads, psc_plan** out);
+/* The same inspection with the window mining on GPU `device` (one thread per
+ * window, the three strategies of miner.cpp:298-320, cuda/inspect.cu); the
+ * schedule and windows are computed on the host. Returns the same plan as
+ * psc_inspect, bit for bit. */
+PSC_API psc_status psc_inspect_device(int32_t kernel, const psc_csr_view* a, int32_t t,
+                                      int32_t target_groups, int32_t device, psc_plan** out);
 PSC_API psc_status psc_plan_get_counts(const psc_plan* plan, psc_plan_counts* out);
 /* Mined plans keep their tables implicit (verbatim slices of col_indices,
  * miner.cpp:156-164, 206-226), so export needs the matrix they came from. */

@@ -112,6 +112,7 @@ class ExecContext(Structure):
 _SIGS = {
     "psc_last_error": (c_char_p, []),
     "psc_inspect": (c_int32, [c_int32, POINTER(CsrView), c_int32, c_int32, c_int32, POINTER(c_void_p)]),
+    "psc_inspect_device": (c_int32, [c_int32, POINTER(CsrView), c_int32, c_int32, c_int32, POINTER(c_void_p)]),
     "psc_plan_get_counts": (c_int32, [c_void_p, POINTER(PlanCounts)]),
     "psc_plan_to_arrays": (c_int32, [c_void_p, POINTER(CsrView), POINTER(PlanArrays)]),
     "psc_plan_from_arrays": (c_int32, [POINTER(PlanCounts), POINTER(PlanArrays), POINTER(c_void_p)]),

@@ -52,41 +52,70 @@ Csr csr_from_triplets(int32_t n_rows, int32_t n_cols, std::vector<Triplet> entri
     return a;
 }
 
+namespace {
+// The first row (in row order) for which bad(row) returns a nonzero code,
+// searched over row blocks on every host thread: the same row -- and so the
+// same error -- as a sequential scan.
+template <class F>
+std::pair<int32_t, int> first_bad_row(int32_t n_rows, F&& bad) {
+    constexpr int32_t kBlock = 1 << 16;
+    const int64_t n_blocks = (static_cast<int64_t>(n_rows) + kBlock - 1) / kBlock;
+    std::vector<std::pair<int32_t, int>> found(static_cast<std::size_t>(n_blocks), {-1, 0});
+    parallel_for(n_blocks, hw_threads(0), [&](int64_t b) {
+        const int32_t r0 = static_cast<int32_t>(b * kBlock);
+        const int32_t r1 = static_cast<int32_t>(std::min<int64_t>(n_rows, r0 + static_cast<int64_t>(kBlock)));
+        for (int32_t row = r0; row < r1; ++row) {
+            if (const int code = bad(row)) {
+                found[b] = {row, code};
+                return;
+            }
+        }
+    });
+    for (const auto& f : found)
+        if (f.first >= 0) return f;
+    return {-1, 0};
+}
+}  // namespace
+
 void validate_csr(const psc_csr_view& a) {
     require(a.n_rows >= 0 && a.n_cols >= 0, "csr: negative dimension");
     require(a.row_offsets != nullptr, "csr: row_offsets size mismatch");
     require(a.row_offsets[0] == 0 && a.row_offsets[a.n_rows] == a.nnz,
             "csr: row_offsets endpoints mismatch");
     require(a.nnz <= INT32_MAX, "csr: more than 2^31-1 stored entries");
-    for (int32_t row = 0; row < a.n_rows; ++row) {
-        int32_t b = a.row_offsets[row], e = a.row_offsets[row + 1];
-        if (b > e) throw std::invalid_argument("csr: row_offsets not monotone at row " + std::to_string(row));
+    const auto [row, code] = first_bad_row(a.n_rows, [&](int32_t r) {
+        const int32_t b = a.row_offsets[r], e = a.row_offsets[r + 1];
+        if (b > e) return 1;
         for (int32_t k = b; k < e; ++k) {
-            int32_t c = a.col_indices[k];
-            if (c < 0 || c >= a.n_cols)
-                throw std::invalid_argument("csr: column out of range in row " + std::to_string(row));
-            if (k > b && c <= a.col_indices[k - 1])
-                throw std::invalid_argument("csr: columns not strictly increasing in row " +
-                                            std::to_string(row));
+            const int32_t c = a.col_indices[k];
+            if (c < 0 || c >= a.n_cols) return 2;
+            if (k > b && c <= a.col_indices[k - 1]) return 3;
         }
-    }
+        return 0;
+    });
+    if (code == 1) throw std::invalid_argument("csr: row_offsets not monotone at row " + std::to_string(row));
+    if (code == 2) throw std::invalid_argument("csr: column out of range in row " + std::to_string(row));
+    if (code == 3) throw std::invalid_argument("csr: columns not strictly increasing in row " + std::to_string(row));
 }
 
 void adopt_triangular(const psc_csr_view& a) {
     validate_csr(a);
     require(a.n_rows == a.n_cols, "triangular: matrix not square");
-    for (int32_t row = 0; row < a.n_rows; ++row) {
-        for (int32_t k = a.row_offsets[row]; k < a.row_offsets[row + 1]; ++k) {
-            if (a.col_indices[k] > row) throw std::invalid_argument("triangular: entry above the diagonal");
-        }
-    }
-    for (int32_t row = 0; row < a.n_rows; ++row) {
-        int32_t last = a.row_offsets[row + 1] - 1;
-        if (last < a.row_offsets[row] || a.col_indices[last] != row)
-            throw std::invalid_argument("triangular: missing diagonal at row " + std::to_string(row));
-        if (a.values[last] == 0.0)
-            throw std::invalid_argument("triangular: zero diagonal at row " + std::to_string(row));
-    }
+    // every entry above the diagonal is reported before any diagonal problem
+    if (first_bad_row(a.n_rows, [&](int32_t r) {
+            for (int32_t k = a.row_offsets[r]; k < a.row_offsets[r + 1]; ++k)
+                if (a.col_indices[k] > r) return 1;
+            return 0;
+        }).second)
+        throw std::invalid_argument("triangular: entry above the diagonal");
+    const auto [row, code] = first_bad_row(a.n_rows, [&](int32_t r) {
+        const int32_t last = a.row_offsets[r + 1] - 1;
+        if (last < a.row_offsets[r] || a.col_indices[last] != r) return 1;
+        if (a.values[last] == 0.0) return 2;
+        return 0;
+    });
+    if (code == 1) throw std::invalid_argument("triangular: missing diagonal at row " + std::to_string(row));
+    if (code == 2) throw std::invalid_argument("triangular: zero diagonal at row " + std::to_string(row));
 }
 
 Csr lower_triangular(const psc_csr_view& a) {

@@ -183,7 +183,7 @@ struct BlockResult {
 
 }  // namespace
 
-Plan inspect(int kernel, const psc_csr_view& a, int t, int target_groups, int threads) {
+WindowSchedule schedule_windows(int kernel, const psc_csr_view& a, int t, int target_groups) {
     require(t >= 1, "inspect: t must be >= 1");
     require(target_groups >= 1, "inspect: target_groups must be >= 1");
     require(kernel == PSC_KERNEL_SPMV || kernel == PSC_KERNEL_SPTRSV, "inspect: unknown kernel");
@@ -193,7 +193,6 @@ Plan inspect(int kernel, const psc_csr_view& a, int t, int target_groups, int th
     } else {
         validate_csr(a);
     }
-    threads = hw_threads(threads);
     const int n = a.n_rows;
     const int32_t* ro = a.row_offsets;
     Model md{ro, a.col_indices, kernel == PSC_KERNEL_SPTRSV ? 1 : 0};
@@ -249,14 +248,28 @@ Plan inspect(int kernel, const psc_csr_view& a, int t, int target_groups, int th
 
     // ---- windows ----
     std::vector<Window> windows;
-    std::vector<int64_t> part_win_ptr{0};
+    WindowSchedule ws;
     windows.reserve(static_cast<std::size_t>(n / t + n_parts + 1));
     for (int64_t p = 0; p < n_parts; ++p) {
         consecutive_windows(part_rows.data() + part_ptr[p], part_ptr[p + 1] - part_ptr[p], t, windows);
-        part_win_ptr.push_back(static_cast<int64_t>(windows.size()));
+        ws.part_win_ptr.push_back(static_cast<int64_t>(windows.size()));
     }
-    part_rows.clear();
-    part_rows.shrink_to_fit();
+    ws.begin.resize(windows.size());
+    ws.end.resize(windows.size());
+    for (std::size_t w = 0; w < windows.size(); ++w) {
+        ws.begin[w] = windows[w].begin;
+        ws.end[w] = windows[w].end;
+    }
+    return ws;
+}
+
+Plan inspect(int kernel, const psc_csr_view& a, int t, int target_groups, int threads) {
+    WindowSchedule ws = schedule_windows(kernel, a, t, target_groups);
+    threads = hw_threads(threads);
+    Model md{a.row_offsets, a.col_indices, kernel == PSC_KERNEL_SPTRSV ? 1 : 0};
+    std::vector<Window> windows(ws.begin.size());
+    for (std::size_t w = 0; w < windows.size(); ++w) windows[w] = {ws.begin[w], ws.end[w]};
+    const std::vector<int64_t>& part_win_ptr = ws.part_win_ptr;
 
     // ---- mine every window (miner.cpp:298-320), in parallel blocks ----
     const int64_t n_win = static_cast<int64_t>(windows.size());

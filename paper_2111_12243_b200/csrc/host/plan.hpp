@@ -70,6 +70,19 @@ struct Plan {
 // inspect (miner.cpp:281-323), bit-exact.
 Plan inspect(int kernel, const psc_csr_view& a, int t, int target_groups, int threads);
 
+// The schedule and windows of inspect (compute_access_functions validation,
+// scheduler.cpp:9-105, get_consecutive_iterations miner.cpp:18-37): window w
+// covers rows [begin[w], end[w]); partition p owns windows
+// [part_win_ptr[p], part_win_ptr[p + 1]).
+struct WindowSchedule {
+    std::vector<int32_t> begin, end;
+    std::vector<int64_t> part_win_ptr{0};
+};
+WindowSchedule schedule_windows(int kernel, const psc_csr_view& a, int t, int target_groups);
+
+// inspect with the window mining on a GPU (cuda/inspect.cu): the same plan.
+Plan inspect_device(int kernel, const psc_csr_view& a, int t, int target_groups, int device);
+
 void plan_counts(const Plan& p, psc_plan_counts* c);
 void plan_to_arrays(const Plan& p, const psc_csr_view* a, psc_plan_arrays* out);
 Plan plan_from_arrays(const psc_plan_counts& c, const psc_plan_arrays& a);

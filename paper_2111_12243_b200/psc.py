@@ -611,6 +611,14 @@ def inspect(kernel, a: CsrMatrix, t: int, target_groups: int, threads: int = 0) 
     return CodeletPlan(h, a)
 
 
+def inspect_device(kernel, a: CsrMatrix, t: int, target_groups: int, device: int = 0) -> CodeletPlan:
+    """inspect with the window mining on GPU `device` (psc_inspect_device):
+    the same plan as inspect(), bit for bit."""
+    h = C.c_void_p()
+    _check(_capi.lib().psc_inspect_device(int(kernel), C.byref(a.view()), t, target_groups, device, C.byref(h)))
+    return CodeletPlan(h, a)
+
+
 def validate_plan(plan: CodeletPlan, a: CsrMatrix) -> None:
     _check(_capi.lib().psc_validate_plan(plan.handle, C.byref(a.view())))
 

@@ -362,3 +362,36 @@ def test_peer_exchange_real_ipc_two_processes():
     for it in range(2):
         got = np.concatenate([res[r][it] for r in range(world)])
         assert bitwise_equal(got, want)
+
+
+# ---- GPU inspector (psc_inspect_device): the same plans as the host inspector ----
+
+def test_device_inspector_acceptance_suite():
+    """Every plan of the acceptance suite (42 cases x t x groups) mined on the
+    GPU has the host inspector's digest (which is pinned to the reference's
+    own inspector in test_oracle.py)."""
+    n = 0
+    for name, kernel, a, _ in suite_cases():
+        for t in (1, 2, 3, 8):
+            for groups in (1, 4):
+                want = P.inspect(kernel, a, t, groups).hash()
+                got = P.inspect_device(kernel, a, t, groups).hash()
+                assert got == want, f"{name} t={t} groups={groups}"
+                n += 1
+    assert n == 336
+
+
+@pytest.mark.parametrize("config,scale,kernel", [
+    (1, 1.0, KernelKind.Spmv),
+    (2, 1.0, KernelKind.Sptrsv),
+    (3, 0.2, KernelKind.Spmv),
+    (4, 0.5, KernelKind.Sptrsv),
+    (5, 0.05, KernelKind.Spmv),
+])
+def test_device_inspector_configs(config, scale, kernel):
+    a = P.generate_config(config, scale)
+    host = P.inspect(kernel, a, 3, 8)
+    dev = P.inspect_device(kernel, a, 3, 8)
+    assert dev.hash() == host.hash()
+    assert dev.counts().n_codelets == host.counts().n_codelets
+    assert dev.totals() == host.totals()
