@@ -13,7 +13,7 @@ cap() {  # config kernel-regex name
 }
 cap 2 sptrsv_rec c2_sptrsv_rec
 cap 1 spmv_row c1_spmv_row
-cap 3 spmv_segquad c3_spmv_segquad
-cap 4 sptrsv_queue c4_sptrsv_queue
+cap 3 spmv_group c3_spmv_group
+cap 4 sptrsv_stream c4_sptrsv_stream
 cap 5 spmv_chunk c5_spmv_chunk
 ls -la gpurun_out/prof
