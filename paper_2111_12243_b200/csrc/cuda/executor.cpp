@@ -86,6 +86,11 @@ struct psc_bound {
     DevBuf rsp, sst, slen, svec, chunk_row, item_seg, long_list, ticket, armed;
     DevBuf groups;      // SpMV row groups {r0, g} (segmented plans)
     int n_groups = 0;
+    // column-split SpMV (kernels.hpp SplitPassDev): two CSRs by column half,
+    // their chunks and long rows, and the rows' dot_unit state between passes
+    bool split = false;
+    DevBuf sp_ro[2], sp_col[2], sp_val[2], sp_items[2], sp_long[2], sp_state;
+    int sp_n_items[2] = {0, 0}, sp_n_long[2] = {0, 0};
     bool chain_mode = false;
     int max_block_units = 0;
     DevBuf block_row, block_unit, unit_start;
@@ -143,7 +148,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &sp_ro[0], &sp_ro[1], &sp_col[0], &sp_col[1], &sp_val[0], &sp_val[1], &sp_items[0], &sp_items[1], &sp_long[0], &sp_long[1], &sp_state, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -176,8 +181,66 @@ std::vector<int32_t> fingerprint(const psc_csr_view& a) {
 
 // Build a bound plan. force_general lowers through the exact interpreter
 // (execute_plan semantics need accumulate-onto-existing for the solve).
+// Column-split SpMV: two CSRs -- entries with column < n_cols / 2, then the
+// rest (columns are sorted within a row, so each row splits at one point) --
+// each chunked like the plan's rows (<= 256 entries and rows per chunk,
+// longer rows alone). Values are bound once (psc_bind: the run_* API, which
+// re-uploads values per call, does not split).
+void build_split(psc_bound* b, const psc_csr_view& a, cudaStream_t s) {
+    const int32_t n = a.n_rows, split = a.n_cols / 2;
+    const int32_t* ro = a.row_offsets;
+    std::vector<int32_t> ka(n);
+    parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
+        for (int32_t r = static_cast<int32_t>(blk * 65536); r < std::min<int64_t>(n, (blk + 1) * 65536); ++r)
+            ka[r] = static_cast<int32_t>(std::lower_bound(a.col_indices + ro[r], a.col_indices + ro[r + 1], split) -
+                                         a.col_indices);
+    });
+    for (int q = 0; q < 2; ++q) {
+        std::vector<int32_t> pro(static_cast<size_t>(n) + 1, 0);
+        for (int32_t r = 0; r < n; ++r) pro[r + 1] = pro[r] + (q == 0 ? ka[r] - ro[r] : ro[r + 1] - ka[r]);
+        const int64_t m = pro[n];
+        std::vector<int32_t> pc(static_cast<size_t>(m));
+        std::vector<double> pv(static_cast<size_t>(m));
+        parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
+            for (int32_t r = static_cast<int32_t>(blk * 65536); r < std::min<int64_t>(n, (blk + 1) * 65536); ++r) {
+                const int32_t k0 = q == 0 ? ro[r] : ka[r], k1 = q == 0 ? ka[r] : ro[r + 1];
+                std::copy(a.col_indices + k0, a.col_indices + k1, pc.begin() + pro[r]);
+                std::copy(a.values + k0, a.values + k1, pv.begin() + pro[r]);
+            }
+        });
+        std::vector<int32_t> items, longs;
+        int32_t c0 = 0;
+        auto close = [&](int32_t r1) {
+            if (r1 > c0) items.insert(items.end(), {c0, r1, pro[c0], pro[r1]});
+        };
+        for (int32_t r = 0; r < n; ++r) {
+            if (pro[r + 1] - pro[r] > kSpmvWarpCap) {
+                close(r);
+                longs.push_back(r);
+                c0 = r + 1;
+                continue;
+            }
+            if (pro[r + 1] - pro[c0] > kSpmvWarpCap || r + 1 - c0 > kSpmvWarpCap) {
+                close(r);
+                c0 = r;
+            }
+        }
+        close(n);
+        b->sp_ro[q].upload(pro, s);
+        b->sp_col[q].upload(pc, s);
+        b->sp_val[q].upload(pv, s);
+        b->sp_items[q].upload(items, s);
+        b->sp_long[q].upload(longs, s);
+        b->sp_n_items[q] = static_cast<int>(items.size() / 4);
+        b->sp_n_long[q] = static_cast<int>(longs.size());
+        ck(cudaStreamSynchronize(s), "split upload");  // the host staging vectors go out of scope
+    }
+    b->sp_state.ensure(static_cast<size_t>(n) * 4 * sizeof(double));
+    b->split = true;
+}
+
 std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_view& a, int mode, int64_t p0,
-                                      int64_t p1, bool force_general, cudaStream_t s) {
+                                      int64_t p1, bool force_general, cudaStream_t s, bool allow_split = false) {
     if (p.kernel == PSC_KERNEL_SPTRSV) adopt_triangular(a);
     else validate_csr(a);
     Lowered L = lower_plan(p, a, p0, p1, 0, force_general);
@@ -217,6 +280,13 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->n_chunks = static_cast<int>(L.items.size() / 4);
             b->groups.upload(L.groups, s);
             b->n_groups = static_cast<int>(L.groups.size() / 8);
+            // x of at least PSC_SPMV_SPLIT_BYTES (default: about an L2) -> column-split passes
+            // (a negative threshold disables them)
+            if (allow_split && L.simple && L.row_begin == 0 && L.row_end == a.n_rows) {
+                const char* v = std::getenv("PSC_SPMV_SPLIT_BYTES");
+                const int64_t min_bytes = v ? std::atoll(v) : 128000000LL;
+                if (min_bytes >= 0 && static_cast<int64_t>(a.n_cols) * 8 >= min_bytes) build_split(b.get(), a, s);
+            }
             b->long_rows = L.long_rows;
             // every row of a simple plan <= 16 entries: thread-per-row kernel (PSC_SPMV_ROWK=0 disables)
             if (L.simple && L.long_rows == 0) {
@@ -468,7 +538,19 @@ void run_general(psc_bound* b, const double* gather, double* accum, const double
 
 void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     use_device(b->device);
-    if (b->canonical) {
+    if (b->canonical && b->split) {
+        SplitPassDev P[2];
+        for (int q = 0; q < 2; ++q) {
+            P[q].ro_pass = b->sp_ro[q].as<int32_t>();
+            P[q].col = b->sp_col[q].as<int32_t>();
+            P[q].val = b->sp_val[q].as<double>();
+            P[q].items = b->sp_items[q].as<int4>();
+            P[q].n_items = b->sp_n_items[q];
+            P[q].long_rows = b->sp_long[q].as<int32_t>();
+            P[q].n_long = b->sp_n_long[q];
+        }
+        launch_spmv_split(b->ro.as<int32_t>(), P[0], P[1], b->sp_state.as<double>(), x, y, false, b->n_sms, s);
+    } else if (b->canonical) {
         launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
                            b->chunk_row.as<int4>(), b->n_chunks, b->item_seg.as<int2>(), b->long_list.as<int32_t>(),
                            static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, b->spmv_short, b->rows(), s);
@@ -578,7 +660,7 @@ PSC_API psc_status psc_bind(psc_executor* e, const psc_plan* plan, const psc_csr
         require(e && plan && a && out, "bind: null argument");
         require(mode == PSC_MODE_PARITY || mode == PSC_MODE_FAST, "bind: unknown mode");
         std::lock_guard<std::mutex> lk(e->mu);
-        *out = make_bound(e->device, plan->p, *a, mode, -1, -1, false, e->stream).release();
+        *out = make_bound(e->device, plan->p, *a, mode, -1, -1, false, e->stream, true).release();
     });
 }
 PSC_API psc_status psc_bind_partitions(psc_executor* e, const psc_plan* plan, const psc_csr_view* a, int32_t mode,
@@ -840,6 +922,8 @@ PSC_API int32_t psc_bound_launches(const psc_bound* b) {
     if (!b) return 0;
     if (b->canonical) {
         if (b->kernel != PSC_KERNEL_SPMV) return 1;
+        if (b->split)
+            return (b->sp_n_long[0] > 0) + (b->sp_n_items[0] > 0) + (b->sp_n_long[1] > 0) + (b->sp_n_items[1] > 0);
         const int n = (b->long_rows > 0) + (b->n_chunks > 0) + (b->n_groups > 0);
         return n > 0 ? n : 1;
     }

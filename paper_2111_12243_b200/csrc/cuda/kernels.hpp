@@ -45,6 +45,23 @@ struct PeerDev {
 // {row begin, row end, CSR begin, CSR end} (<= 256 entries and rows each) with
 // their segment ranges item_seg (segmented plans); long_rows: rows with more
 // than 256 entries (kernels.cu "SpMV parity kernels"). Up to two launches.
+// Column-split SpMV (simple plans whose x outgrows L2): the matrix stored as
+// two CSRs, entries with column < split and the rest, multiplied in two
+// passes, each gathering from one half of x. A row's dot_unit state (its
+// four lane sums, or its running tail sum) crosses from pass 0 to pass 1
+// through `state` (4 doubles per row). ro: the full matrix's row offsets.
+struct SplitPassDev {
+    const int32_t* ro_pass = nullptr;  // this pass's CSR
+    const int32_t* col = nullptr;
+    const double* val = nullptr;
+    const int4* items = nullptr;       // chunks {r0, r1, k0, k1} in this pass's CSR
+    int n_items = 0;
+    const int32_t* long_rows = nullptr;  // rows with more than 256 entries in this pass
+    int n_long = 0;
+};
+void launch_spmv_split(const int32_t* ro, const SplitPassDev& pass0, const SplitPassDev& pass1, double* state,
+                       const double* x, double* y, bool accumulate, int n_sms, cudaStream_t stream);
+
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                         double* y, const int4* items, int n_items, const int2* item_seg,
                         const int32_t* long_rows, int n_long, SegmentsDev segs, bool accumulate, int n_sms,

@@ -200,3 +200,43 @@ def test_spmv_row_groups(monkeypatch, groups):
     monkeypatch.setenv("PSC_SPMV_GROUPS", groups)
     exe = P.Executor(1)
     _spmv_check(exe, _block_rows_matrix())
+
+
+@pytest.mark.parametrize("force", [True, False])
+def test_spmv_column_split(monkeypatch, force):
+    """Column-split passes (the matrix as two CSRs by column half, the rows'
+    dot_unit state carried between the passes): power-law rows with long
+    rows, empty rows, rows entirely in one half, and rows whose lane sums /
+    tail straddle the split. Bitwise against the oracle with the split forced
+    on (PSC_SPMV_SPLIT_BYTES=1) and off."""
+    import torch
+
+    monkeypatch.setenv("PSC_SPMV_SPLIT_BYTES", "1" if force else "-1")
+    exe = P.Executor(1)
+    rng = np.random.default_rng(31)
+    n = 3000
+    ent = []
+    for r in range(n):
+        k = int(min(2000, rng.zipf(1.8))) if r % 11 else 0  # every 11th row empty
+        if r % 13 == 1:
+            cols = rng.choice(n // 2, size=min(k + 3, n // 2), replace=False)  # low half only
+        elif r % 13 == 2:
+            cols = n // 2 + rng.choice(n - n // 2, size=min(k + 3, n // 2), replace=False)  # high half only
+        elif r % 7 == 3:  # long rows straddling the split: unaligned starts, tails across pieces
+            lo = (1, 2, 3, 5, 255, 257, 701)[(r // 7) % 7]
+            hi = (257, 258, 259, 513, 515, 600)[(r // 49) % 6]
+            cols = np.arange(max(0, n // 2 - lo), min(n, n // 2 + hi))
+        else:
+            cols = rng.choice(n, size=min(k, n), replace=False)
+        ent += [(r, int(c), float(rng.uniform(-1, 1))) for c in cols]
+    a = _csr(n, n, ent)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(n, 5)
+    want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+    bound = P.BoundPlan(exe, plan, a)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    for _ in range(2):  # the state buffer is reused across calls
+        bound.spmv(xd, yd)
+    torch.cuda.synchronize()
+    assert bitwise_equal(yd.cpu().numpy(), want)
