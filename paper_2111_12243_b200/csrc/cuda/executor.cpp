@@ -88,9 +88,10 @@ struct psc_bound {
     int n_groups = 0;
     // column-split SpMV (kernels.hpp SplitPassDev): two CSRs by column half,
     // their chunks and long rows, and the rows' dot_unit state between passes
-    bool split = false;
-    DevBuf sp_ro[2], sp_col[2], sp_val[2], sp_items[2], sp_long[2], sp_state;
-    int sp_n_items[2] = {0, 0}, sp_n_long[2] = {0, 0};
+    int split = 0;  // column-split passes (0: none)
+    DevBuf sp_j0[kMaxSplitPasses], sp_ro[kMaxSplitPasses], sp_col[kMaxSplitPasses], sp_val[kMaxSplitPasses],
+        sp_items[kMaxSplitPasses], sp_long[kMaxSplitPasses], sp_state;
+    int sp_n_items[kMaxSplitPasses] = {}, sp_n_long[kMaxSplitPasses] = {};
     bool chain_mode = false;
     int max_block_units = 0;
     DevBuf block_row, block_unit, unit_start;
@@ -148,7 +149,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &sp_ro[0], &sp_ro[1], &sp_col[0], &sp_col[1], &sp_val[0], &sp_val[1], &sp_items[0], &sp_items[1], &sp_long[0], &sp_long[1], &sp_state, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &sp_ro[0], &sp_ro[1], &sp_ro[2], &sp_ro[3], &sp_col[0], &sp_col[1], &sp_col[2], &sp_col[3], &sp_val[0], &sp_val[1], &sp_val[2], &sp_val[3], &sp_j0[1], &sp_j0[2], &sp_j0[3], &sp_state, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -186,26 +187,33 @@ std::vector<int32_t> fingerprint(const psc_csr_view& a) {
 // each chunked like the plan's rows (<= 256 entries and rows per chunk,
 // longer rows alone). Values are bound once (psc_bind: the run_* API, which
 // re-uploads values per call, does not split).
-void build_split(psc_bound* b, const psc_csr_view& a, cudaStream_t s) {
-    const int32_t n = a.n_rows, split = a.n_cols / 2;
+void build_split(psc_bound* b, const psc_csr_view& a, int parts, cudaStream_t s) {
+    const int32_t n = a.n_rows;
     const int32_t* ro = a.row_offsets;
-    std::vector<int32_t> ka(n);
-    parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
-        for (int32_t r = static_cast<int32_t>(blk * 65536); r < std::min<int64_t>(n, (blk + 1) * 65536); ++r)
-            ka[r] = static_cast<int32_t>(std::lower_bound(a.col_indices + ro[r], a.col_indices + ro[r + 1], split) -
-                                         a.col_indices);
-    });
-    for (int q = 0; q < 2; ++q) {
-        std::vector<int32_t> pro(static_cast<size_t>(n) + 1, 0);
-        for (int32_t r = 0; r < n; ++r) pro[r + 1] = pro[r] + (q == 0 ? ka[r] - ro[r] : ro[r + 1] - ka[r]);
+    // kb[q][r]: row r's first entry with column >= q * n_cols / parts (columns are sorted in a row)
+    std::vector<std::vector<int32_t>> kb(static_cast<size_t>(parts) + 1, std::vector<int32_t>(n));
+    for (int q = 0; q <= parts; ++q) {
+        const int32_t c = static_cast<int32_t>(static_cast<int64_t>(a.n_cols) * q / parts);
+        parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
+            for (int32_t r = static_cast<int32_t>(blk * 65536); r < std::min<int64_t>(n, (blk + 1) * 65536); ++r)
+                kb[q][r] = q == 0 ? ro[r] : q == parts ? ro[r + 1] :
+                           static_cast<int32_t>(std::lower_bound(a.col_indices + ro[r], a.col_indices + ro[r + 1], c) -
+                                                a.col_indices);
+        });
+    }
+    for (int q = 0; q < parts; ++q) {
+        std::vector<int32_t> pro(static_cast<size_t>(n) + 1, 0), j0(n);
+        for (int32_t r = 0; r < n; ++r) {
+            pro[r + 1] = pro[r] + (kb[q + 1][r] - kb[q][r]);
+            j0[r] = kb[q][r] - ro[r];
+        }
         const int64_t m = pro[n];
         std::vector<int32_t> pc(static_cast<size_t>(m));
         std::vector<double> pv(static_cast<size_t>(m));
         parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
             for (int32_t r = static_cast<int32_t>(blk * 65536); r < std::min<int64_t>(n, (blk + 1) * 65536); ++r) {
-                const int32_t k0 = q == 0 ? ro[r] : ka[r], k1 = q == 0 ? ka[r] : ro[r + 1];
-                std::copy(a.col_indices + k0, a.col_indices + k1, pc.begin() + pro[r]);
-                std::copy(a.values + k0, a.values + k1, pv.begin() + pro[r]);
+                std::copy(a.col_indices + kb[q][r], a.col_indices + kb[q + 1][r], pc.begin() + pro[r]);
+                std::copy(a.values + kb[q][r], a.values + kb[q + 1][r], pv.begin() + pro[r]);
             }
         });
         std::vector<int32_t> items, longs;
@@ -226,6 +234,7 @@ void build_split(psc_bound* b, const psc_csr_view& a, cudaStream_t s) {
             }
         }
         close(n);
+        if (q > 0) b->sp_j0[q].upload(j0, s);
         b->sp_ro[q].upload(pro, s);
         b->sp_col[q].upload(pc, s);
         b->sp_val[q].upload(pv, s);
@@ -236,7 +245,7 @@ void build_split(psc_bound* b, const psc_csr_view& a, cudaStream_t s) {
         ck(cudaStreamSynchronize(s), "split upload");  // the host staging vectors go out of scope
     }
     b->sp_state.ensure(static_cast<size_t>(n) * 4 * sizeof(double));
-    b->split = true;
+    b->split = parts;
 }
 
 std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_view& a, int mode, int64_t p0,
@@ -285,7 +294,15 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             if (allow_split && L.simple && L.row_begin == 0 && L.row_end == a.n_rows) {
                 const char* v = std::getenv("PSC_SPMV_SPLIT_BYTES");
                 const int64_t min_bytes = v ? std::atoll(v) : 128000000LL;
-                if (min_bytes >= 0 && static_cast<int64_t>(a.n_cols) * 8 >= min_bytes) build_split(b.get(), a, s);
+                if (min_bytes >= 0 && static_cast<int64_t>(a.n_cols) * 8 >= min_bytes) {
+                    // parts of x of at most ~60 MB each (config 5, x = 160 MB: 2 / 3 / 4 parts:
+                    // 3.54 / 3.45 / 3.63 ms, unsplit 4.67 ms), 2..4 passes
+                    const char* pv = std::getenv("PSC_SPMV_SPLIT_PARTS");
+                    int parts = pv ? std::atoi(pv)
+                                   : static_cast<int>((static_cast<int64_t>(a.n_cols) * 8 + 59999999) / 60000000);
+                    parts = std::max(2, std::min(kMaxSplitPasses, parts));
+                    build_split(b.get(), a, parts, s);
+                }
             }
             b->long_rows = L.long_rows;
             // every row of a simple plan <= 16 entries: thread-per-row kernel (PSC_SPMV_ROWK=0 disables)
@@ -539,8 +556,9 @@ void run_general(psc_bound* b, const double* gather, double* accum, const double
 void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     use_device(b->device);
     if (b->canonical && b->split) {
-        SplitPassDev P[2];
-        for (int q = 0; q < 2; ++q) {
+        SplitPassDev P[kMaxSplitPasses];
+        for (int q = 0; q < b->split; ++q) {
+            P[q].j0 = q > 0 ? b->sp_j0[q].as<int32_t>() : nullptr;
             P[q].ro_pass = b->sp_ro[q].as<int32_t>();
             P[q].col = b->sp_col[q].as<int32_t>();
             P[q].val = b->sp_val[q].as<double>();
@@ -549,7 +567,7 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
             P[q].long_rows = b->sp_long[q].as<int32_t>();
             P[q].n_long = b->sp_n_long[q];
         }
-        launch_spmv_split(b->ro.as<int32_t>(), P[0], P[1], b->sp_state.as<double>(), x, y, false, b->n_sms, s);
+        launch_spmv_split(b->ro.as<int32_t>(), P, b->split, b->sp_state.as<double>(), x, y, false, b->n_sms, s);
     } else if (b->canonical) {
         launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
                            b->chunk_row.as<int4>(), b->n_chunks, b->item_seg.as<int2>(), b->long_list.as<int32_t>(),
@@ -922,8 +940,11 @@ PSC_API int32_t psc_bound_launches(const psc_bound* b) {
     if (!b) return 0;
     if (b->canonical) {
         if (b->kernel != PSC_KERNEL_SPMV) return 1;
-        if (b->split)
-            return (b->sp_n_long[0] > 0) + (b->sp_n_items[0] > 0) + (b->sp_n_long[1] > 0) + (b->sp_n_items[1] > 0);
+        if (b->split) {
+            int n = 0;
+            for (int q = 0; q < b->split; ++q) n += (b->sp_n_long[q] > 0) + (b->sp_n_items[q] > 0);
+            return n;
+        }
         const int n = (b->long_rows > 0) + (b->n_chunks > 0) + (b->n_groups > 0);
         return n > 0 ? n : 1;
     }

@@ -46,11 +46,13 @@ struct PeerDev {
 // their segment ranges item_seg (segmented plans); long_rows: rows with more
 // than 256 entries (kernels.cu "SpMV parity kernels"). Up to two launches.
 // Column-split SpMV (simple plans whose x outgrows L2): the matrix stored as
-// two CSRs, entries with column < split and the rest, multiplied in two
-// passes, each gathering from one half of x. A row's dot_unit state (its
-// four lane sums, or its running tail sum) crosses from pass 0 to pass 1
-// through `state` (4 doubles per row). ro: the full matrix's row offsets.
+// one CSR per column range, multiplied in passes that each gather from one
+// range of x. A row's dot_unit state (its four lane sums, or its running tail
+// sum) crosses from pass to pass through `state` (4 doubles per row). ro:
+// the full matrix's row offsets.
+constexpr int kMaxSplitPasses = 4;
 struct SplitPassDev {
+    const int32_t* j0 = nullptr;       // per row: index of its first entry in this pass (null: 0)
     const int32_t* ro_pass = nullptr;  // this pass's CSR
     const int32_t* col = nullptr;
     const double* val = nullptr;
@@ -59,8 +61,8 @@ struct SplitPassDev {
     const int32_t* long_rows = nullptr;  // rows with more than 256 entries in this pass
     int n_long = 0;
 };
-void launch_spmv_split(const int32_t* ro, const SplitPassDev& pass0, const SplitPassDev& pass1, double* state,
-                       const double* x, double* y, bool accumulate, int n_sms, cudaStream_t stream);
+void launch_spmv_split(const int32_t* ro, const SplitPassDev* passes, int n_passes, double* state, const double* x,
+                       double* y, bool accumulate, int n_sms, cudaStream_t stream);
 
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                         double* y, const int4* items, int n_items, const int2* item_seg,

@@ -202,16 +202,17 @@ def test_spmv_row_groups(monkeypatch, groups):
     _spmv_check(exe, _block_rows_matrix())
 
 
-@pytest.mark.parametrize("force", [True, False])
-def test_spmv_column_split(monkeypatch, force):
+@pytest.mark.parametrize("force,parts", [(True, "2"), (True, "3"), (True, "4"), (False, "2")])
+def test_spmv_column_split(monkeypatch, force, parts):
     """Column-split passes (the matrix as two CSRs by column half, the rows'
-    dot_unit state carried between the passes): power-law rows with long
+    dot_unit state carried between the passes; 2, 3 or 4 column ranges): power-law rows with long
     rows, empty rows, rows entirely in one half, and rows whose lane sums /
     tail straddle the split. Bitwise against the oracle with the split forced
     on (PSC_SPMV_SPLIT_BYTES=1) and off."""
     import torch
 
     monkeypatch.setenv("PSC_SPMV_SPLIT_BYTES", "1" if force else "-1")
+    monkeypatch.setenv("PSC_SPMV_SPLIT_PARTS", parts)
     exe = P.Executor(1)
     rng = np.random.default_rng(31)
     n = 3000
