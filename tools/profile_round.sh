@@ -15,5 +15,5 @@ cap 2 sptrsv_rec c2_sptrsv_rec
 cap 1 spmv_row c1_spmv_row
 cap 3 spmv_group c3_spmv_group
 cap 4 sptrsv_stream c4_sptrsv_stream
-cap 5 spmv_chunk c5_spmv_chunk
+cap 5 spmv_split_chunk c5_spmv_split_chunk
 ls -la gpurun_out/prof
