@@ -241,3 +241,8 @@ def test_spmv_column_split(monkeypatch, force, parts):
         bound.spmv(xd, yd)
     torch.cuda.synchronize()
     assert bitwise_equal(yd.cpu().numpy(), want)
+    yh = np.full(n, np.nan)
+    bound.spmv_host(x, yh)  # host-buffer path (H2D x, passes, D2H y)
+    torch.cuda.synchronize()
+    assert bitwise_equal(yh, want)
+    assert bound.launches() >= (2 if force else 1)
