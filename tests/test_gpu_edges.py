@@ -246,3 +246,58 @@ def test_spmv_column_split(monkeypatch, force, parts):
     torch.cuda.synchronize()
     assert bitwise_equal(yh, want)
     assert bound.launches() >= (2 if force else 1)
+
+
+def test_spmv_side_stream_concurrent_threads(monkeypatch):
+    """Plans that fork work onto the side stream (row groups beside chunks,
+    long rows beside chunks, column-split passes) driven from five host
+    threads at once, each on its own CUDA stream with its own bound plan; x
+    changes on the caller's stream before every call, so a side-stream launch
+    that ran ahead of its fork would read a stale x. Bitwise per call."""
+    import threading
+
+    import torch
+
+    exe = P.Executor(1)
+    a_groups = _block_rows_matrix()
+    rng = np.random.default_rng(41)
+    n = 2000
+    ent = []
+    for r in range(n):
+        k = 300 if r % 97 == 0 else 6  # long rows (> 256 entries) among chunk rows
+        ent += [(r, int(c), float(rng.uniform(-1, 1))) for c in rng.choice(n, size=k, replace=False)]
+    a_long = _csr(n, n, ent)
+    jobs = []
+    for a, split in ((a_groups, "-1"), (a_long, "-1"), (a_long, "1"), (a_groups, "-1"), (a_long, "1")):
+        monkeypatch.setenv("PSC_SPMV_SPLIT_BYTES", split)  # read at bind: "1" forces the split passes
+        plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+        xs = [P.uniform_vector(a.n_cols, 100 + i) for i in range(4)]
+        want = [Oracle.run_spmv(plan.export_arrays(), a.view(), x) for x in xs]
+        jobs.append((P.BoundPlan(exe, plan, a), xs, want))
+    iters = 40
+    monkeypatch.setenv("PSC_SPMV_SPLIT_BYTES", "-1")
+    results = [None] * len(jobs)
+
+    def run(j):
+        bound, xs, _ = jobs[j]
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            xsd = [torch.from_numpy(x).cuda() for x in xs]
+            xd = torch.empty_like(xsd[0])
+            yd = torch.empty(len(jobs[j][2][0]), dtype=torch.float64, device="cuda")
+            out = torch.empty((iters, yd.numel()), dtype=torch.float64, device="cuda")
+            for i in range(iters):
+                xd.copy_(xsd[i % len(xs)])
+                bound.spmv(xd, yd, stream=s)
+                out[i].copy_(yd)
+        s.synchronize()
+        results[j] = out.cpu().numpy()
+
+    threads = [threading.Thread(target=run, args=(j,)) for j in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for j, (_, xs, want) in enumerate(jobs):
+        for i in range(iters):
+            assert bitwise_equal(results[j][i], want[i % len(xs)]), (j, i)
