@@ -323,6 +323,7 @@ def run_ours(args):
 
     # ---- parity against the C oracle, once, before timing ----
     parity = "unchecked"
+    got = None
     try:
         from oracle.oracle import Oracle
 
@@ -374,6 +375,7 @@ def run_ours(args):
     kern_ms = np.array([m.elapsed_time(e) for _, m, e in ev])
 
     # ---- e2e: host buffers through the C ABI (H2D input, kernel, D2H result) ----
+    e2e_parity = "unchecked"
     if sharded:
         e2e_ms = step_ms.copy()  # x already device-resident per rank; reported as the exchange+compute step
         h2d = d2h = 0
@@ -393,6 +395,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_ms = np.array([s.elapsed_time(e) for s, e in e2e_ev])
         h2d, d2h = 8 * a.n_cols, 8 * rows
+        if got is not None and rows > 0:  # the host-buffer result against the device path's (oracle-checked) one
+            e2e_parity = ("bitwise (equal to the device path)"
+                          if np.array_equal(hout[:rows].view(np.int64), got.view(np.int64)) else "MISMATCH")
     sampler.stop()
 
     ms_step = float(step_ms.mean())
@@ -450,7 +455,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": total_flops * (1 if sharded else world) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                "path": "psc_bound_*_host (pinned host buffers; SpTRSV: b gathered from mapped host memory unit by unit in level order during the solve, x shipped per finished unit by bulk copies)"},
+                "path": "psc_bound_*_host (pinned host buffers; SpTRSV: b gathered from mapped host memory unit by unit in level order during the solve, x shipped per finished unit by bulk copies; column-split SpMV: x uploaded range by range ahead of its pass, y sent down per row slice of the last pass)",
+                "parity": e2e_parity},
         "gpu_launches": args.steps * bound.launches(),
         "clocks": clocks,
         "inspector_seconds": inspector_s,

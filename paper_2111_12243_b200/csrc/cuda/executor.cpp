@@ -116,6 +116,10 @@ struct psc_bound {
     // overlapped upload of b (host path, record kernel): copy stream, chunk flags
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_before = nullptr, ev_copied = nullptr;
+    cudaEvent_t ev_part[kMaxSplitPasses] = {};  // host path, column split: x range q landed
+    static constexpr int kYSlices = 4;             // ... and the last pass in row slices, y of each sent down at once
+    int32_t ysl_row[kYSlices + 1] = {}, ysl_item[kYSlices + 1] = {}, ysl_long[kYSlices + 1] = {};
+    cudaEvent_t ev_slice[kYSlices] = {};
     DevBuf b_ready, g_order;  // host path: per-unit arrival flags (+ gather ticket), gather order
     int n_units_total = 0;
     int* flag_patterns = nullptr;  // pinned, immutable: [i] = 0x01010101 * i (flags are written by the copy engine)
@@ -124,6 +128,10 @@ struct psc_bound {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (ev_before) cudaEventDestroy(ev_before);
         if (ev_copied) cudaEventDestroy(ev_copied);
+        for (cudaEvent_t e : ev_part)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_slice)
+            if (e) cudaEventDestroy(e);
     }
     // general path
     std::vector<int64_t> part_group_ptr;
@@ -234,6 +242,18 @@ void build_split(psc_bound* b, const psc_csr_view& a, int parts, cudaStream_t s)
             }
         }
         close(n);
+        if (q == parts - 1) {  // row slices of the last pass, cut at item starts (host path: y goes down per slice)
+            const int n_it = static_cast<int>(items.size() / 4);
+            for (int i = 0; i <= psc_bound::kYSlices; ++i) {
+                const int64_t t = static_cast<int64_t>(n) * i / psc_bound::kYSlices;
+                int ia = 0;
+                while (ia < n_it && items[4 * static_cast<size_t>(ia)] < t) ++ia;
+                const int32_t cut = i == psc_bound::kYSlices ? n : ia < n_it ? items[4 * static_cast<size_t>(ia)] : n;
+                b->ysl_row[i] = cut;
+                b->ysl_item[i] = i == psc_bound::kYSlices ? n_it : ia;
+                b->ysl_long[i] = static_cast<int>(std::lower_bound(longs.begin(), longs.end(), cut) - longs.begin());
+            }
+        }
         if (q > 0) b->sp_j0[q].upload(j0, s);
         b->sp_ro[q].upload(pro, s);
         b->sp_col[q].upload(pc, s);
@@ -553,20 +573,24 @@ void run_general(psc_bound* b, const double* gather, double* accum, const double
     ck(cudaGetLastError(), "general kernel launch");
 }
 
+void split_passes(const psc_bound* b, SplitPassDev (&P)[kMaxSplitPasses]) {
+    for (int q = 0; q < b->split; ++q) {
+        P[q].j0 = q > 0 ? b->sp_j0[q].as<int32_t>() : nullptr;
+        P[q].ro_pass = b->sp_ro[q].as<int32_t>();
+        P[q].col = b->sp_col[q].as<int32_t>();
+        P[q].val = b->sp_val[q].as<double>();
+        P[q].items = b->sp_items[q].as<int4>();
+        P[q].n_items = b->sp_n_items[q];
+        P[q].long_rows = b->sp_long[q].as<int32_t>();
+        P[q].n_long = b->sp_n_long[q];
+    }
+}
+
 void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     use_device(b->device);
     if (b->canonical && b->split) {
         SplitPassDev P[kMaxSplitPasses];
-        for (int q = 0; q < b->split; ++q) {
-            P[q].j0 = q > 0 ? b->sp_j0[q].as<int32_t>() : nullptr;
-            P[q].ro_pass = b->sp_ro[q].as<int32_t>();
-            P[q].col = b->sp_col[q].as<int32_t>();
-            P[q].val = b->sp_val[q].as<double>();
-            P[q].items = b->sp_items[q].as<int4>();
-            P[q].n_items = b->sp_n_items[q];
-            P[q].long_rows = b->sp_long[q].as<int32_t>();
-            P[q].n_long = b->sp_n_long[q];
-        }
+        split_passes(b, P);
         launch_spmv_split(b->ro.as<int32_t>(), P, b->split, b->sp_state.as<double>(), x, y, false, b->n_sms, s);
     } else if (b->canonical) {
         launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
@@ -838,9 +862,64 @@ PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x, double* y,
         require(b->kernel == PSC_KERNEL_SPMV, "run_spmv: plan was built for another kernel");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         use_device(b->device);
-        b->hx.upload_raw(x, static_cast<size_t>(b->n_cols) * sizeof(double), s);
         b->hy.ensure(std::max(1, b->rows()) * sizeof(double));
-        bound_spmv(b, b->hx.as<double>(), b->hy.as<double>(), s);
+        if (b->canonical && b->split) {
+            // Column-split passes: pass q reads only x's column range q, so the
+            // ranges go up on a copy stream one by one and pass q waits for its
+            // own; the upload of the later ranges hides the earlier passes.
+            if (!b->copy_stream) {
+                ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&b->ev_before, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&b->ev_copied, cudaEventDisableTiming), "event");
+            }
+            for (int q = 0; q < b->split; ++q)
+                if (!b->ev_part[q]) ck(cudaEventCreateWithFlags(&b->ev_part[q], cudaEventDisableTiming), "event");
+            b->hx.ensure(std::max<size_t>(8, static_cast<size_t>(b->n_cols) * sizeof(double)));
+            ck(cudaEventRecord(b->ev_before, s), "event");  // earlier work on s is done with hx
+            ck(cudaStreamWaitEvent(b->copy_stream, b->ev_before, 0), "wait");
+            for (int q = 0; q < b->split; ++q) {  // the column ranges of build_split
+                const int64_t c0 = static_cast<int64_t>(b->n_cols) * q / b->split;
+                const int64_t c1 = static_cast<int64_t>(b->n_cols) * (q + 1) / b->split;
+                if (c1 > c0)
+                    ck(cudaMemcpyAsync(b->hx.as<double>() + c0, x + c0, static_cast<size_t>(c1 - c0) * sizeof(double),
+                                       cudaMemcpyHostToDevice, b->copy_stream), "H2D");
+                ck(cudaEventRecord(b->ev_part[q], b->copy_stream), "event");
+            }
+            SplitPassDev P[kMaxSplitPasses];
+            split_passes(b, P);
+            const int last = b->split - 1;
+            for (int q = 0; q < last; ++q) {
+                ck(cudaStreamWaitEvent(s, b->ev_part[q], 0), "wait");
+                launch_spmv_split(b->ro.as<int32_t>(), P, q + 1, b->sp_state.as<double>(), b->hx.as<double>(),
+                                  b->hy.as<double>(), false, b->n_sms, s, q);
+            }
+            // the last pass slice by slice; each slice's y rows are final once it ran
+            ck(cudaStreamWaitEvent(s, b->ev_part[last], 0), "wait");
+            const SplitPassDev whole = P[last];
+            for (int i = 0; i < psc_bound::kYSlices; ++i) {
+                if (!b->ev_slice[i]) ck(cudaEventCreateWithFlags(&b->ev_slice[i], cudaEventDisableTiming), "event");
+                P[last].items = whole.items + b->ysl_item[i];
+                P[last].n_items = b->ysl_item[i + 1] - b->ysl_item[i];
+                P[last].long_rows = whole.long_rows + b->ysl_long[i];
+                P[last].n_long = b->ysl_long[i + 1] - b->ysl_long[i];
+                launch_spmv_split(b->ro.as<int32_t>(), P, last + 1, b->sp_state.as<double>(), b->hx.as<double>(),
+                                  b->hy.as<double>(), false, b->n_sms, s, last);
+                const int32_t r0 = b->ysl_row[i], r1 = b->ysl_row[i + 1];
+                if (r1 > r0) {
+                    ck(cudaEventRecord(b->ev_slice[i], s), "event");
+                    ck(cudaStreamWaitEvent(b->copy_stream, b->ev_slice[i], 0), "wait");
+                    ck(cudaMemcpyAsync(y + r0, b->hy.as<double>() + r0, static_cast<size_t>(r1 - r0) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, b->copy_stream), "D2H");
+                }
+            }
+            ck(cudaEventRecord(b->ev_copied, b->copy_stream), "event");
+            ck(cudaStreamWaitEvent(s, b->ev_copied, 0), "wait");  // the caller's stream covers the copies
+            ck(cudaGetLastError(), "spmv launch");
+            return;
+        } else {
+            b->hx.upload_raw(x, static_cast<size_t>(b->n_cols) * sizeof(double), s);
+            bound_spmv(b, b->hx.as<double>(), b->hy.as<double>(), s);
+        }
         ck(cudaMemcpyAsync(y, b->hy.p, static_cast<size_t>(b->rows()) * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     });
 }

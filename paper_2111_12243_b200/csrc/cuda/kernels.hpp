@@ -61,8 +61,10 @@ struct SplitPassDev {
     const int32_t* long_rows = nullptr;  // rows with more than 256 entries in this pass
     int n_long = 0;
 };
+// passes [pass_begin, n_passes) of a column-split multiply (the ones before
+// must already have run on `stream`)
 void launch_spmv_split(const int32_t* ro, const SplitPassDev* passes, int n_passes, double* state, const double* x,
-                       double* y, bool accumulate, int n_sms, cudaStream_t stream);
+                       double* y, bool accumulate, int n_sms, cudaStream_t stream, int pass_begin = 0);
 
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                         double* y, const int4* items, int n_items, const int2* item_seg,
