@@ -301,3 +301,34 @@ def test_spmv_side_stream_concurrent_threads(monkeypatch):
     for j, (_, xs, want) in enumerate(jobs):
         for i in range(iters):
             assert bitwise_equal(results[j][i], want[i % len(xs)]), (j, i)
+
+
+@pytest.mark.parametrize("n,band", [(5, 2), (1000, 3), (100003, 40), (20000, None)])
+def test_spmv_host_row_slices(n, band):
+    """Host-buffer SpMV (`psc_bound_spmv_host`) of thread-per-row plans:
+    banded rows, a 5-row matrix, random columns, empty rows. Bitwise against
+    the oracle, twice in a row (the second call reuses the scratch buffers)."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    ent = []
+    for r in range(n):
+        if band is None:
+            cols = rng.choice(n, size=min(n, 7), replace=False)
+        else:
+            cols = [c for c in range(r - band, r + band + 1, max(1, band // 3)) if 0 <= c < n]
+        if r % 17 == 5:
+            cols = []  # empty rows
+        ent += [(r, int(c), float(rng.uniform(-1, 1))) for c in cols]
+    a = _csr(n, n, ent)
+    exe = P.Executor(1)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    bound = P.BoundPlan(exe, plan, a)
+    for seed in (1, 2):
+        x = P.uniform_vector(n, seed)
+        want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+        xh = torch.from_numpy(x).pin_memory().numpy()
+        yh = torch.full((n,), float("nan"), dtype=torch.float64).pin_memory().numpy()
+        bound.spmv_host(xh, yh)
+        torch.cuda.synchronize()
+        assert bitwise_equal(yh, want), seed
