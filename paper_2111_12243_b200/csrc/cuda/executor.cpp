@@ -44,7 +44,8 @@ struct DevBuf {
     void ensure(size_t n) {
         if (n <= bytes && p) return;
         release();
-        ck(cudaMalloc(&p, std::max<size_t>(n, 16)), "cudaMalloc");
+        // +64 bytes: 16-byte-rounded bulk copies of a tail stay in bounds (spmv_fast.cu)
+        ck(cudaMalloc(&p, std::max<size_t>(n, 16) + 64), "cudaMalloc");
         bytes = std::max<size_t>(n, 16);
     }
     template <class T>
@@ -92,6 +93,14 @@ struct psc_bound {
     DevBuf sp_j0[kMaxSplitPasses], sp_ro[kMaxSplitPasses], sp_col[kMaxSplitPasses], sp_val[kMaxSplitPasses],
         sp_items[kMaxSplitPasses], sp_long[kMaxSplitPasses], sp_state;
     int sp_n_items[kMaxSplitPasses] = {}, sp_n_long[kMaxSplitPasses] = {};
+    // fast mode (simple SpMV, spmv_fast.cu): flagged entry streams, one per
+    // column range of x (one range unless x outgrows the L2)
+    int fast_passes = 0;  // 0: fast mode not in use
+    int32_t fp_c0[kMaxSplitPasses + 1] = {};  // column ranges of the passes
+    DevBuf fl_colf[kMaxSplitPasses], fl_val[kMaxSplitPasses], fl_m0[kMaxSplitPasses], fp_carry_val, fp_carry_row;
+    int64_t fl_n_ent[kMaxSplitPasses] = {};
+    int fl_n_chunks[kMaxSplitPasses] = {};
+    int fl_per = 4;  // entries per lane (PSC_FAST_PER: 4 or 8)
     bool chain_mode = false;
     int max_block_units = 0;
     DevBuf block_row, block_unit, unit_start;
@@ -161,6 +170,9 @@ struct psc_bound {
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
+        t += fp_carry_val.bytes + fp_carry_row.bytes;
+        for (int q = 0; q < kMaxSplitPasses; ++q)
+            t += fl_colf[q].bytes + fl_val[q].bytes + fl_m0[q].bytes;
         return static_cast<int64_t>(t);
     }
 };
@@ -268,6 +280,99 @@ void build_split(psc_bound* b, const psc_csr_view& a, int parts, cudaStream_t s)
     b->split = parts;
 }
 
+// Fast mode over the bound rows (local CSR: ro[0..n] rebased, col/val from
+// a.col_indices/values + k_begin): one pass over the whole CSR, or `parts`
+// column ranges each stored as its own CSR (columns are sorted within a row,
+// so a row splits at one point per range boundary).
+void build_fast(psc_bound* b, const psc_csr_view& a, const std::vector<int32_t>& ro, int parts, cudaStream_t s) {
+    const int32_t n = b->rows();
+    const int32_t* col = a.col_indices + b->k_begin;
+    const double* val = a.values + b->k_begin;
+    if (const char* h = std::getenv("PSC_FAST_PER")) b->fl_per = std::atoi(h) == 8 ? 8 : 4;
+    parts = std::max(1, parts);
+    int64_t max_chunks = 0;
+    std::vector<int32_t> lo(n), hi(n);
+    for (int q = 0; q < parts; ++q) {
+        const int32_t c0 = static_cast<int32_t>(static_cast<int64_t>(a.n_cols) * q / parts);
+        const int32_t c1 = static_cast<int32_t>(static_cast<int64_t>(a.n_cols) * (q + 1) / parts);
+        b->fp_c0[q] = c0;
+        b->fp_c0[q + 1] = c1;
+        // row r's entries in column range q: [lo[r], hi[r]) (columns are sorted in a row)
+        parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
+            const int32_t r1 = static_cast<int32_t>(std::min<int64_t>(n, (blk + 1) * 65536));
+            for (int32_t r = static_cast<int32_t>(blk * 65536); r < r1; ++r) {
+                const int32_t* rb = col + ro[r];
+                const int32_t* re = col + ro[r + 1];
+                lo[r] = q == 0 ? ro[r] : static_cast<int32_t>(std::lower_bound(rb, re, c0) - col);
+                hi[r] = q == parts - 1 ? ro[r + 1] : static_cast<int32_t>(std::lower_bound(rb, re, c1) - col);
+            }
+        });
+        {
+            // entries in CSR order, bit 31 of the column on each row's last entry; a
+            // row with no entries in this pass gets one placeholder (column
+            // 0x7fffffff, value 0) so that row end m is row m; per chunk, the row
+            // ends before it; padded to whole chunks (lanes load 16-byte vectors)
+            const int64_t ch = flag_chunk_entries(b->fl_per);
+            std::vector<int64_t> fo(static_cast<size_t>(n) + 1, 0);
+            for (int32_t r = 0; r < n; ++r) fo[r + 1] = fo[r] + std::max(1, hi[r] - lo[r]);
+            const int64_t mf = fo[n];
+            const size_t m_pad = static_cast<size_t>((mf + ch - 1) / ch * ch);
+            std::vector<int32_t> colf(m_pad, 0);
+            std::vector<double> pv(m_pad, 0.0);
+            parallel_for((n + 65535) / 65536, hw_threads(0), [&](int64_t blk) {
+                const int32_t r1 = static_cast<int32_t>(std::min<int64_t>(n, (blk + 1) * 65536));
+                for (int32_t r = static_cast<int32_t>(blk * 65536); r < r1; ++r) {
+                    if (hi[r] > lo[r]) {
+                        std::copy(col + lo[r], col + hi[r], colf.begin() + fo[r]);
+                        std::copy(val + lo[r], val + hi[r], pv.begin() + fo[r]);
+                    } else {
+                        colf[fo[r]] = 0x7fffffff;
+                    }
+                    colf[fo[r + 1] - 1] |= static_cast<int32_t>(0x80000000u);
+                }
+            });
+            const int64_t n_chunks = (mf + ch - 1) / ch;
+            require(n_chunks < INT32_MAX && mf < INT32_MAX, "bind: too many fast-mode entries");
+            std::vector<int32_t> m0(static_cast<size_t>(std::max<int64_t>(1, n_chunks)));
+            {   // row ends before chunk c = the number of rows ending before entry c * ch
+                int32_t r = 0;
+                for (int64_t c = 0; c < n_chunks; ++c) {
+                    while (r < n && fo[r + 1] <= c * ch) ++r;
+                    m0[c] = r;
+                }
+            }
+            b->fl_colf[q].upload(colf, s);
+            b->fl_val[q].upload(pv, s);
+            b->fl_m0[q].upload(m0, s);
+            b->fl_n_ent[q] = mf;
+            b->fl_n_chunks[q] = static_cast<int>(n_chunks);
+            max_chunks = std::max<int64_t>(max_chunks, n_chunks);
+        }
+        ck(cudaStreamSynchronize(s), "fast upload");  // the staging vectors go out of scope
+    }
+    b->fp_carry_val.ensure(static_cast<size_t>(std::max<int64_t>(1, max_chunks)) * sizeof(double));
+    b->fp_carry_row.ensure(static_cast<size_t>(std::max<int64_t>(1, max_chunks)) * sizeof(int32_t));
+    b->fast_passes = parts;
+}
+
+FlagPassDev flag_pass(const psc_bound* b, int q) {
+    FlagPassDev P;
+    P.colf = b->fl_colf[q].as<int32_t>();
+    P.val = b->fl_val[q].as<double>();
+    P.chunk_m0 = b->fl_m0[q].as<int32_t>();
+    P.n_ent = b->fl_n_ent[q];
+    P.n_chunks = b->fl_n_chunks[q];
+    P.per = b->fl_per;
+    P.carry_val = b->fp_carry_val.as<double>();
+    P.carry_row = b->fp_carry_row.as<int32_t>();
+    return P;
+}
+
+// pass q of a fast multiply
+void fast_pass_launch(const psc_bound* b, int q, const double* x, double* y, cudaStream_t s) {
+    launch_spmv_flag(flag_pass(b, q), x, y, q > 0, b->n_sms, s);
+}
+
 std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_view& a, int mode, int64_t p0,
                                       int64_t p1, bool force_general, cudaStream_t s, bool allow_split = false) {
     if (p.kernel == PSC_KERNEL_SPTRSV) adopt_triangular(a);
@@ -311,7 +416,17 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->n_groups = static_cast<int>(L.groups.size() / 8);
             // x of at least PSC_SPMV_SPLIT_BYTES (default: about an L2) -> column-split passes
             // (a negative threshold disables them)
-            if (allow_split && L.simple && L.row_begin == 0 && L.row_end == a.n_rows) {
+            if (mode == PSC_MODE_FAST && L.simple) {
+                // fast mode: merge-path tiles; column ranges of <= PSC_FAST_SPLIT_BYTES
+                // of x each once x outgrows the L2 (a negative value: never split)
+                const char* v = std::getenv("PSC_FAST_SPLIT_BYTES");
+                // (config 5, x = 160 MB: 2 / 3 / 4 ranges 2.27 / 2.05 / 2.31 ms; one range 4.9 ms)
+                const int64_t part_bytes = v ? std::atoll(v) : 55000000LL;
+                const int64_t xb = static_cast<int64_t>(a.n_cols) * 8;
+                int parts = part_bytes > 0 && xb > 100000000LL ? static_cast<int>((xb + part_bytes - 1) / part_bytes) : 1;
+                parts = std::max(1, std::min(kMaxSplitPasses, parts));
+                build_fast(b.get(), a, ro, parts, s);
+            } else if (allow_split && L.simple && L.row_begin == 0 && L.row_end == a.n_rows) {
                 const char* v = std::getenv("PSC_SPMV_SPLIT_BYTES");
                 const int64_t min_bytes = v ? std::atoll(v) : 128000000LL;
                 if (min_bytes >= 0 && static_cast<int64_t>(a.n_cols) * 8 >= min_bytes) {
@@ -588,7 +703,9 @@ void split_passes(const psc_bound* b, SplitPassDev (&P)[kMaxSplitPasses]) {
 
 void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     use_device(b->device);
-    if (b->canonical && b->split) {
+    if (b->canonical && b->fast_passes) {
+        for (int q = 0; q < b->fast_passes; ++q) fast_pass_launch(b, q, x, y, s);
+    } else if (b->canonical && b->split) {
         SplitPassDev P[kMaxSplitPasses];
         split_passes(b, P);
         launch_spmv_split(b->ro.as<int32_t>(), P, b->split, b->sp_state.as<double>(), x, y, false, b->n_sms, s);
@@ -863,7 +980,33 @@ PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x, double* y,
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         use_device(b->device);
         b->hy.ensure(std::max(1, b->rows()) * sizeof(double));
-        if (b->canonical && b->split) {
+        if (b->canonical && b->fast_passes > 1) {
+            // fast column-split passes: x range q goes up on the copy stream and
+            // pass q waits only for it, so the later ranges' upload hides the
+            // earlier passes
+            if (!b->copy_stream) {
+                ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&b->ev_before, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&b->ev_copied, cudaEventDisableTiming), "event");
+            }
+            for (int q = 0; q < b->fast_passes; ++q)
+                if (!b->ev_part[q]) ck(cudaEventCreateWithFlags(&b->ev_part[q], cudaEventDisableTiming), "event");
+            b->hx.ensure(std::max<size_t>(8, static_cast<size_t>(b->n_cols) * sizeof(double)));
+            ck(cudaEventRecord(b->ev_before, s), "event");  // earlier work on s is done with hx
+            ck(cudaStreamWaitEvent(b->copy_stream, b->ev_before, 0), "wait");
+            for (int q = 0; q < b->fast_passes; ++q) {
+                const int64_t c0 = b->fp_c0[q], c1 = b->fp_c0[q + 1];
+                if (c1 > c0)
+                    ck(cudaMemcpyAsync(b->hx.as<double>() + c0, x + c0, static_cast<size_t>(c1 - c0) * sizeof(double),
+                                       cudaMemcpyHostToDevice, b->copy_stream), "H2D");
+                ck(cudaEventRecord(b->ev_part[q], b->copy_stream), "event");
+            }
+            for (int q = 0; q < b->fast_passes; ++q) {
+                ck(cudaStreamWaitEvent(s, b->ev_part[q], 0), "wait");
+                fast_pass_launch(b, q, b->hx.as<double>(), b->hy.as<double>(), s);
+            }
+            ck(cudaGetLastError(), "spmv launch");
+        } else if (b->canonical && b->split) {
             // Column-split passes: pass q reads only x's column range q, so the
             // ranges go up on a copy stream one by one and pass q waits for its
             // own; the upload of the later ranges hides the earlier passes.
@@ -1019,6 +1162,7 @@ PSC_API int32_t psc_bound_launches(const psc_bound* b) {
     if (!b) return 0;
     if (b->canonical) {
         if (b->kernel != PSC_KERNEL_SPMV) return 1;
+        if (b->fast_passes) return 2 * b->fast_passes;
         if (b->split) {
             int n = 0;
             for (int q = 0; q < b->split; ++q) n += (b->sp_n_long[q] > 0) + (b->sp_n_items[q] > 0);

@@ -66,6 +66,26 @@ struct SplitPassDev {
 void launch_spmv_split(const int32_t* ro, const SplitPassDev* passes, int n_passes, double* state, const double* x,
                        double* y, bool accumulate, int n_sms, cudaStream_t stream, int pass_begin = 0);
 
+// Fast mode (spmv_fast.cu spmv_flag_kernel), one pass: the pass's
+// entries in CSR order with bit 31 of the column set on each row's last
+// entry (a row without entries in the pass holds one placeholder, column
+// 0x7fffffff), and per chunk of flag_chunk_entries() entries the number of
+// row ends before it.
+struct FlagPassDev {
+    const int32_t* colf = nullptr;
+    const double* val = nullptr;
+    const int32_t* chunk_m0 = nullptr;
+    int64_t n_ent = 0;
+    int n_chunks = 0;
+    int per = 8;  // entries per lane (a chunk is 32 * per entries)
+    double* carry_val = nullptr;
+    int32_t* carry_row = nullptr;
+};
+int flag_chunk_entries(int per);
+// y = (accumulate ? y : 0) + A_pass x; two launches (chunks, then the carries).
+void launch_spmv_flag(const FlagPassDev& pass, const double* x, double* y, bool accumulate, int n_sms,
+                      cudaStream_t stream);
+
 void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                         double* y, const int4* items, int n_items, const int2* item_seg,
                         const int32_t* long_rows, int n_long, SegmentsDev segs, bool accumulate, int n_sms,
