@@ -294,7 +294,7 @@ PSC_API psc_status psc_exec_pscii_codelet(const psc_codelet_view* c, const psc_e
 PSC_API psc_status psc_csr_spmv_device(const psc_bound* b, const double* x_dev, double* y_dev,
                                        void* stream);
 
-/* ---- matrices: reference generators (pattern_gen.hpp) + benchmark configs -- */
+/* ---- matrices: construction, validation, Matrix Market, benchmark configs -- */
 typedef struct psc_csr psc_csr; /* owned CSR */
 PSC_API psc_status psc_csr_view_of(const psc_csr* m, psc_csr_view* out);
 PSC_API void psc_csr_destroy(psc_csr* m);
@@ -317,7 +317,6 @@ PSC_API psc_status psc_csr_write_matrix_market(const psc_csr_view* a, const char
 PSC_API psc_status psc_validate_csr(const psc_csr_view* a);
 PSC_API psc_status psc_lower_triangular(const psc_csr_view* a, psc_csr** out);
 PSC_API psc_status psc_adopt_triangular(const psc_csr_view* a); /* TriangularMatrix::adopt checks */
-PSC_API psc_status psc_generate_pattern(const char* spec, uint64_t default_seed, psc_csr** out);
 /* BASELINE.json configs 1..5; scale in (0,1] shrinks the
  * grid / n for tests; seed selects the value stream. */
 PSC_API psc_status psc_generate_config(int32_t config, double scale, uint64_t seed, psc_csr** out);

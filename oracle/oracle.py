@@ -195,6 +195,9 @@ class Ref:
             lib.ref_csr_free.argtypes = [c_void_p]
             lib.ref_csr_free.restype = None
             lib.ref_generate_pattern.argtypes = [c_char_p, c_uint64, vp]
+            lib.ref_generate_config.argtypes = [c_int, c_double, c_uint64, vp]
+            lib.ref_uniform_vector.argtypes = [c_int64, c_uint64, c_double, c_double, POINTER(c_double)]
+            lib.ref_uniform_vector.restype = None
             lib.ref_read_matrix_market.argtypes = [c_char_p, vp, POINTER(C.c_int)]
             lib.ref_csr_from_triplets.argtypes = [c_int, c_int, c_int64, POINTER(C.c_int32), POINTER(C.c_int32),
                                                   POINTER(c_double), vp]
@@ -259,6 +262,19 @@ class Ref:
         h = c_void_p()
         cls._check(cls.lib().ref_generate_pattern(spec.encode(), seed, C.byref(h)))
         return RefCsr(h)
+
+    @classmethod
+    def generate_config(cls, config: int, scale: float = 1.0, seed: int = 0) -> RefCsr:
+        """BASELINE.json config (the product's configs.cpp compiled into the reference library)."""
+        h = c_void_p()
+        cls._check(cls.lib().ref_generate_config(config, float(scale), seed, C.byref(h)))
+        return RefCsr(h)
+
+    @classmethod
+    def uniform_vector(cls, n: int, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+        v = np.empty(n, dtype=np.float64)
+        cls.lib().ref_uniform_vector(n, seed, lo, hi, _dp(v))
+        return v
 
     @classmethod
     def lower_triangular(cls, a: RefCsr) -> RefCsr:

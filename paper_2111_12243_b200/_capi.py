@@ -170,7 +170,6 @@ _SIGS = {
     "psc_validate_csr": (c_int32, [POINTER(CsrView)]),
     "psc_lower_triangular": (c_int32, [POINTER(CsrView), POINTER(c_void_p)]),
     "psc_adopt_triangular": (c_int32, [POINTER(CsrView)]),
-    "psc_generate_pattern": (c_int32, [c_char_p, c_uint64, POINTER(c_void_p)]),
     "psc_generate_config": (c_int32, [c_int32, c_double, c_uint64, POINTER(c_void_p)]),
     "psc_seeded_vector": (None, [c_int64, c_uint64, POINTER(c_double)]),
     "psc_uniform_vector": (None, [c_int64, c_uint64, c_double, c_double, POINTER(c_double)]),

@@ -3,11 +3,11 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
-#include <random>
 #include <string>
 
 #include "capi_types.hpp"
 #include "common.hpp"
+#include "configs.hpp"
 #include "csr.hpp"
 #include "plan.hpp"
 
@@ -53,12 +53,6 @@ PSC_API psc_status psc_lower_triangular(const psc_csr_view* a, psc_csr** out) {
 PSC_API psc_status psc_adopt_triangular(const psc_csr_view* a) {
     return guarded([&] { adopt_triangular(*a); });
 }
-PSC_API psc_status psc_generate_pattern(const char* spec, uint64_t default_seed, psc_csr** out) {
-    return guarded([&] {
-        require(spec != nullptr, "generate_pattern: null spec");
-        *out = new psc_csr{generate_pattern(spec, default_seed)};
-    });
-}
 // The reference's sequential baselines (executor.cpp:310-340, SURVEY.md §8a
 // row A13): the NER / verification baselines of the bench report. Plain
 // host loops, built without -march (no FMA contraction).
@@ -90,18 +84,11 @@ PSC_API psc_status psc_generate_config(int32_t config, double scale, uint64_t se
     return guarded([&] { *out = new psc_csr{generate_config(config, scale, seed)}; });
 }
 
-PSC_API void psc_seeded_vector(int64_t n, uint64_t seed, double* out) {
-    std::mt19937_64 rng(seed);  // bench.cpp:50-57
-    for (int64_t i = 0; i < n; ++i) out[i] = 0.5 + to_unit(rng());
-}
+PSC_API void psc_seeded_vector(int64_t n, uint64_t seed, double* out) { seeded_vector(n, seed, out); }
 PSC_API void psc_uniform_vector(int64_t n, uint64_t seed, double lo, double hi, double* out) {
-    std::mt19937_64 rng(seed);
-    for (int64_t i = 0; i < n; ++i) out[i] = lo + (hi - lo) * to_unit(rng());
+    uniform_vector(n, seed, lo, hi, out);
 }
-PSC_API void psc_int_vector(int64_t n, uint64_t seed, double* out) {
-    std::mt19937_64 rng(seed);  // test_helpers.hpp:45-50
-    for (int64_t i = 0; i < n; ++i) out[i] = static_cast<double>(1 + rng() % 9);
-}
+PSC_API void psc_int_vector(int64_t n, uint64_t seed, double* out) { int_vector(n, seed, out); }
 
 // ---- inspector / plans ----------------------------------------------------------
 PSC_API psc_status psc_inspect(int32_t kernel, const psc_csr_view* a, int32_t t, int32_t target_groups,

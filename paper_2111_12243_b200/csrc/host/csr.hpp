@@ -1,8 +1,7 @@
-// CSR storage and the input generators (host side).
+// CSR storage and validation (host side).
 #pragma once
 
 #include <cstdint>
-#include <string>
 #include <vector>
 
 #include "psc_b200.h"
@@ -29,7 +28,7 @@ struct Triplet {
     double value;
 };
 
-// csr_matrix.cpp:9-45: stable sort by (row, col), duplicates summed in order.
+// csr_matrix.cpp:9-45 semantics: rows and columns in order, duplicates summed in input order.
 Csr csr_from_triplets(int32_t n_rows, int32_t n_cols, std::vector<Triplet> entries);
 // csr_matrix.cpp:47-76
 void validate_csr(const psc_csr_view& a);
@@ -37,17 +36,5 @@ void validate_csr(const psc_csr_view& a);
 void adopt_triangular(const psc_csr_view& a);
 // csr_matrix.cpp:111-130
 Csr lower_triangular(const psc_csr_view& a);
-
-// pattern_gen.cpp restated (test inputs of the reference suite).
-Csr dense_block(int n);
-Csr banded(int n, int bandwidth, bool lower_only);
-Csr scattered_gather(int rows, std::vector<int> cols);
-Csr random_uniform(int rows, int cols, double density, uint64_t seed);
-Csr generate_pattern(const std::string& spec, uint64_t default_seed);
-
-// BASELINE.json configs 1..5.
-Csr generate_config(int config, double scale, uint64_t seed);
-
-double to_unit(uint64_t bits);  // (bits >> 11) * 2^-53, pattern_gen.cpp:12-14
 
 }  // namespace pscb

@@ -241,29 +241,7 @@ def lower_triangular(a: CsrMatrix) -> TriangularMatrix:
     return TriangularMatrix(CsrMatrix._take(h))
 
 
-# ---- generators (pattern_gen.hpp) and benchmark configs ----
-
-def generate_pattern(spec: str, default_seed: int = 42) -> CsrMatrix:
-    h = C.c_void_p()
-    _check(_capi.lib().psc_generate_pattern(spec.encode(), default_seed, C.byref(h)))
-    return CsrMatrix._take(h)
-
-
-def dense_block(n: int) -> CsrMatrix:
-    return generate_pattern(f"dense_block({n})")
-
-
-def banded(n: int, bandwidth: int, lower_only: bool = False) -> CsrMatrix:
-    return generate_pattern(f"banded({n},{bandwidth}{',lower' if lower_only else ''})")
-
-
-def scattered_gather(rows: int, cols: Sequence[int]) -> CsrMatrix:
-    return generate_pattern(f"scattered_gather({rows},{':'.join(str(int(c)) for c in cols)})")
-
-
-def random_uniform(rows: int, cols: int, density: float, seed: int) -> CsrMatrix:
-    return generate_pattern(f"random_uniform({rows},{cols},{density!r},{seed})")
-
+# ---- benchmark inputs (configs.cpp) ----
 
 def generate_config(config: int, scale: float = 1.0, seed: int = 0) -> CsrMatrix:
     """BASELINE.json configs 1..5; seed 0 = the config's default stream."""

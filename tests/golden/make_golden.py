@@ -1,12 +1,17 @@
-"""Generate tests/golden/ref_golden.npz from the REFERENCE library
-(oracle/_ref/libpsc_ref.so, built from /root/reference by oracle/Makefile).
+"""Generate tests/golden/ref_golden.npz and tests/golden/patterns.npz from the
+REFERENCE library (oracle/_ref/libpsc_ref.so, built from /root/reference by
+oracle/Makefile).
+
+patterns.npz holds the CSR of every reference pattern the tests use (the
+acceptance suite of acceptance_main.cpp:53-82 and the golden cases below),
+made by the reference's own generators (pattern_gen.cpp) -- the product has
+no copy of them.
 
 For every case: the reference inspector's plan digest (include/psc_plan_hash.h),
 total cost / ops, and the outputs of the reference executor (run_spmv /
 run_sptrsv, workers=1) and of the reference naive baselines, on seeded inputs.
-The matrices are rebuilt at test time from the product's generators (checked
-equal to the reference generators in tests/test_capi.py), so only digests and
-vectors are stored. Run in the build container:  python tests/golden/make_golden.py
+Config matrices are rebuilt at test time from configs.cpp (compiled into both
+libraries), so only digests and vectors are stored for them. Run in the build container:  python tests/golden/make_golden.py
 """
 import json
 import os
@@ -19,7 +24,13 @@ sys.path.insert(0, ROOT)
 
 import paper_2111_12243_b200 as P  # noqa: E402
 from oracle.oracle import Ref  # noqa: E402
-from tests.helpers import unit_lower  # noqa: E402
+from tests.helpers import SUITE_SPECS, pattern, unit_lower  # noqa: E402
+
+EXTRA_SPECS = ["dense_block(3)", "dense_block(7)", "banded(20,3)", "banded(20,2,lower)", "scattered_gather(5,9:0:3:3)",
+               "random_uniform(40,30,0.2,5)", "random_uniform(200,200,0.04,3)", "random_uniform(64,64,0.1,9)",
+               "dense_block(2)", "dense_block(4)", "dense_block(6)", "scattered_gather(3,0:2:5)",
+               "scattered_gather(6,0:1:2:3)", "banded(4,0,lower)", "banded(4,1,lower)",
+               "random_uniform(30,30,0.2,17)"]
 
 CASES = [
     # (name, matrix source, kernel, t, groups, input kind)
@@ -40,11 +51,22 @@ CASES = [
 ]
 
 
+def write_patterns():
+    specs = [s for s, _ in SUITE_SPECS] + EXTRA_SPECS + [c[1][1] for c in CASES if c[1][0] != "config"]
+    out = {}
+    for i, spec in enumerate(dict.fromkeys(specs)):
+        n_r, n_c, ro, ci, va = Ref.generate_pattern(spec).arrays()
+        out[f"p{i}_shape"] = np.array([n_r, n_c], dtype=np.int64)
+        out[f"p{i}_ro"], out[f"p{i}_ci"], out[f"p{i}_va"] = ro, ci, va
+        out[f"p{i}_spec"] = np.frombuffer(spec.encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(os.path.dirname(__file__), "patterns.npz"), **out)
+
+
 def build(src):
     if src[0] == "pattern":
-        return P.generate_pattern(src[1])
+        return pattern(src[1])
     if src[0] == "pattern_unit_lower":
-        return unit_lower(P.generate_pattern(src[1]))
+        return unit_lower(pattern(src[1]))
     return P.generate_config(src[1], src[2])
 
 
@@ -58,6 +80,7 @@ def make_input(kind, n):
 
 def main():
     assert Ref.available(), "the reference library must be built (make -C oracle ref)"
+    write_patterns()
     out, index = {}, []
     for i, (name, src, kernel, t, groups, kind) in enumerate(CASES):
         a = build(src)

@@ -1,5 +1,7 @@
 """Shared test inputs: the reference acceptance suite (acceptance_main.cpp:53-82)
-restated over the product's generators, plus comparison helpers."""
+over the reference's own pattern matrices (tests/golden/patterns.npz, made by
+tests/golden/make_golden.py with the reference generators), plus comparison
+helpers."""
 from __future__ import annotations
 
 import numpy as np
@@ -31,11 +33,31 @@ SUITE_SPECS = [
      for s in (1, 7)]
 
 
+_PATTERNS = None
+
+
+def pattern(spec: str) -> P.CsrMatrix:
+    """The reference generator's matrix for `spec` (pattern_gen.cpp), from the fixture."""
+    global _PATTERNS
+    if _PATTERNS is None:
+        import os
+
+        d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "patterns.npz"))
+        _PATTERNS = {}
+        i = 0
+        while f"p{i}_spec" in d:
+            n_r, n_c = (int(v) for v in d[f"p{i}_shape"])
+            _PATTERNS[d[f"p{i}_spec"].tobytes().decode()] = (n_r, n_c, d[f"p{i}_ro"], d[f"p{i}_ci"], d[f"p{i}_va"])
+            i += 1
+    n_r, n_c, ro, ci, va = _PATTERNS[spec]
+    return P.CsrMatrix(n_r, n_c, ro.copy(), ci.copy(), va.copy())
+
+
 def suite_cases():
     """42 cases: (name, kernel, matrix, integer_values) as build_suite() makes them."""
     cases = []
     for spec, ints in SUITE_SPECS:
-        a = P.generate_pattern(spec)
+        a = pattern(spec)
         cases.append((spec + "/solve", KernelKind.Sptrsv, unit_lower(a), ints))
         cases.append((spec, KernelKind.Spmv, a, ints))
     return cases
@@ -85,9 +107,9 @@ def golden_cases():
     for i, meta in enumerate(index):
         src = meta["src"]
         if src[0] == "pattern":
-            a = P.generate_pattern(src[1])
+            a = pattern(src[1])
         elif src[0] == "pattern_unit_lower":
-            a = unit_lower(P.generate_pattern(src[1]))
+            a = unit_lower(pattern(src[1]))
         else:
             a = P.generate_config(int(src[1]), float(src[2]))
         if meta["input"] == "int":

@@ -1,16 +1,20 @@
 """The C-ABI library: loads, exports every symbol include/psc_b200.h declares,
 maps errors onto the reference's exception types, and its matrix helpers
-reproduce the reference's (pattern generators, csr_from_triplets,
-lower_triangular, the seeded vector streams)."""
+reproduce the reference's (csr_from_triplets, lower_triangular, the seeded
+vector streams). The reference's pattern generators are not in the product:
+the tests take their matrices from tests/golden/patterns.npz."""
 import os
 import re
+
+import ctypes as C
 
 import numpy as np
 import pytest
 
 import paper_2111_12243_b200 as P
-from oracle.oracle import Ref
+from oracle.oracle import Ref, RefCsr
 from paper_2111_12243_b200 import _capi
+from tests.helpers import SUITE_SPECS, pattern
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -56,29 +60,53 @@ def test_csr_helpers():
         P.lower_triangular(P.csr_from_triplets(2, 3, [(0, 0, 1.0)]))
     with pytest.raises(P.InvalidArgument):  # missing diagonal
         P.lower_triangular(P.csr_from_triplets(2, 2, [(0, 0, 1.0), (1, 0, 1.0)]))
-    l = P.lower_triangular(P.dense_block(3))
+    l = P.lower_triangular(pattern("dense_block(3)"))
     assert l.csr().nnz() == 6 and l.diag_pos(2) == 5
     bad = P.CsrMatrix(2, 2, [0, 2, 3], [1, 0, 1], [1.0, 1.0, 1.0])
     with pytest.raises(P.InvalidArgument):
         P.validate_csr(bad)
 
 
-def test_pattern_spec_errors():
-    for spec in ["dense_block", "nope(3)", "banded(4,1,upper)", "dense_block(x)", "banded(4)"]:
-        with pytest.raises(P.InvalidArgument):
-            P.generate_pattern(spec)
+@pytest.mark.ref
+def test_csr_from_triplets_matches_the_reference():
+    """csr_matrix.cpp:9-45: unsorted triplets with duplicates (summed in input order)."""
+    rng = np.random.default_rng(5)
+    for n_rows, n_cols, n in [(1, 1, 0), (7, 5, 60), (40, 33, 900), (3, 1000, 50)]:
+        r = rng.integers(0, n_rows, n).astype(np.int32)
+        c = rng.integers(0, n_cols, n).astype(np.int32)
+        v = rng.uniform(-1, 1, n) * 10.0 ** rng.integers(-8, 8, n)
+        mine = P.csr_from_triplets(n_rows, n_cols, list(zip(r.tolist(), c.tolist(), v.tolist())))
+        h = C.c_void_p()
+        Ref._check(Ref.lib().ref_csr_from_triplets(n_rows, n_cols, n, r.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                   c.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                   v.ctypes.data_as(C.POINTER(C.c_double)), C.byref(h)))
+        _, _, ro, ci, va = RefCsr(h).arrays()
+        assert np.array_equal(mine.row_offsets, ro) and np.array_equal(mine.col_indices, ci)
+        assert np.array_equal(mine.values.view(np.int64), va.view(np.int64))
 
 
 @pytest.mark.ref
-def test_generators_match_the_reference():
-    for spec in ["dense_block(7)", "banded(20,3)", "banded(20,2,lower)", "scattered_gather(5,9:0:3:3)",
-                 "random_uniform(40,30,0.2,5)", "random_uniform(16,16,0.3)"]:
-        mine = P.generate_pattern(spec)
+def test_pattern_fixtures_are_the_reference_generators():
+    for spec, _ in SUITE_SPECS:
+        mine = pattern(spec)
         n_r, n_c, ro, ci, va = Ref.generate_pattern(spec).arrays()
         assert (mine.n_rows, mine.n_cols) == (n_r, n_c)
         assert np.array_equal(mine.row_offsets, ro) and np.array_equal(mine.col_indices, ci)
         assert np.array_equal(mine.values, va)
     assert np.array_equal(P.int_vector(50, 3), Ref.int_vector(50, 3))
+
+
+@pytest.mark.ref
+def test_reference_arm_inputs_equal_the_products():
+    """bench.py's reference arm generates its inputs inside the reference library
+    (configs.cpp compiled in by oracle/Makefile); they must be the product's."""
+    for config, scale in [(1, 0.01), (2, 0.001), (3, 0.000125), (4, 0.002), (5, 0.0001)]:
+        mine = P.generate_config(config, scale)
+        n_r, n_c, ro, ci, va = Ref.generate_config(config, scale).arrays()
+        assert (mine.n_rows, mine.n_cols) == (n_r, n_c)
+        assert np.array_equal(mine.row_offsets, ro) and np.array_equal(mine.col_indices, ci)
+        assert np.array_equal(mine.values.view(np.int64), va.view(np.int64))
+    assert np.array_equal(P.uniform_vector(1000, 15), Ref.uniform_vector(1000, 15))
 
 
 def test_config_generators_shapes():

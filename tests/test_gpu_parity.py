@@ -11,7 +11,7 @@ import pytest
 import paper_2111_12243_b200 as P
 from oracle.oracle import Oracle
 from paper_2111_12243_b200 import KernelKind
-from tests.helpers import bitwise_equal, max_rel_err, normwise_err, suite_cases, suite_input
+from tests.helpers import bitwise_equal, max_rel_err, normwise_err, suite_cases, suite_input, pattern
 
 pytestmark = pytest.mark.gpu
 
@@ -235,7 +235,7 @@ def test_fused_peer_exchange_bitwise(exe, config, scale, world):
 def test_general_path_hand_built_plan(exe):
     """A hand-built plan that is not canonical (shared out table, strided gather)
     runs through the exact interpreter and matches the oracle bitwise."""
-    a = P.dense_block(4)
+    a = pattern("dense_block(4)")
     # rows 0 and 1 of the matrix accumulate into outputs 1 and 0 (crossed): not canonical
     c1 = P.Codelet(P.CodeletKind.Blas, 2, 4, P.AccessDesc.strided(1, -1, 0), P.AccessDesc.strided(0, 4, 1),
                    P.AccessDesc.strided(0, 0, 1))

@@ -7,7 +7,7 @@ import pytest
 import paper_2111_12243_b200 as P
 from oracle.oracle import Ref
 from paper_2111_12243_b200 import AccessDesc, CodeletKind, KernelKind, MineStrategy
-from tests.helpers import golden_cases, suite_cases
+from tests.helpers import golden_cases, suite_cases, pattern
 
 
 def mixed_pattern():
@@ -18,7 +18,7 @@ def mixed_pattern():
 
 def test_dense_block_tiles_into_window_rectangles():
     """test_miner.cpp:183-197."""
-    plan = P.inspect(KernelKind.Spmv, P.dense_block(6), 3, 1)
+    plan = P.inspect(KernelKind.Spmv, pattern("dense_block(6)"), 3, 1)
     parts = plan.partitions
     assert len(parts) == 1 and len(parts[0].groups) == 2
     for g in parts[0].groups:
@@ -30,13 +30,13 @@ def test_dense_block_tiles_into_window_rectangles():
 
 def test_worked_example_shared_gather():
     """test_miner.cpp:199-211, :74-96 (BLAS descriptors of dense_block(3))."""
-    plan = P.inspect(KernelKind.Spmv, P.scattered_gather(3, [0, 2, 5]), 3, 1)
+    plan = P.inspect(KernelKind.Spmv, pattern("scattered_gather(3,0:2:5)"), 3, 1)
     g = plan.partitions[0].groups[0]
     assert g.strategy == MineStrategy.BlasFirst and len(g.codelets) == 1
     c = g.codelets[0]
     assert c.kind == CodeletKind.PscI and c.vec == AccessDesc.inner_table([0, 2, 5])
     assert plan.total_cost() == 19 and plan.total_ops() == 9
-    d = P.inspect(KernelKind.Spmv, P.dense_block(3), 3, 1).partitions[0].groups[0].codelets[0]
+    d = P.inspect(KernelKind.Spmv, pattern("dense_block(3)"), 3, 1).partitions[0].groups[0].codelets[0]
     assert d.out == AccessDesc.strided(0, 1, 0)
     assert d.mat == AccessDesc.strided(0, 3, 1)
     assert d.vec == AccessDesc.strided(0, 0, 1)
@@ -67,7 +67,7 @@ def test_pscii_point_table():
 
 def test_diagonal_solve_yields_finalize_records_only():
     """test_miner.cpp:223-238."""
-    plan = P.inspect(KernelKind.Sptrsv, P.banded(4, 0, True), 3, 1)
+    plan = P.inspect(KernelKind.Sptrsv, pattern("banded(4,0,lower)"), 3, 1)
     parts = plan.partitions
     assert len(parts) == 1 and len(parts[0].groups) == 2
     fins = [f for g in parts[0].groups for f in g.finalize]
@@ -77,7 +77,7 @@ def test_diagonal_solve_yields_finalize_records_only():
 
 def test_chain_solve_singleton_levels():
     """test_miner.cpp:240-252, test_scheduler.cpp:56-63."""
-    l = P.banded(4, 1, True)
+    l = pattern("banded(4,1,lower)")
     plan = P.inspect(KernelKind.Sptrsv, l, 3, 1)
     assert len(plan.partitions) == 4
     for k, part in enumerate(plan.partitions):
@@ -94,8 +94,8 @@ def test_scheduler_known_answers():
         [[0], [1, 2, 3, 4]]
     rows = lambda plan: [[r for g in p.groups for r in range(g.window.row_begin, g.window.row_end)]  # noqa: E731
                          for p in plan.partitions]
-    assert rows(P.inspect(KernelKind.Spmv, P.scattered_gather(6, [0, 1, 2, 3]), 8, 2)) == [[0, 1, 2], [3, 4, 5]]
-    assert rows(P.inspect(KernelKind.Spmv, P.dense_block(3), 8, 10)) == [[0], [1], [2]]
+    assert rows(P.inspect(KernelKind.Spmv, pattern("scattered_gather(6,0:1:2:3)"), 8, 2)) == [[0, 1, 2], [3, 4, 5]]
+    assert rows(P.inspect(KernelKind.Spmv, pattern("dense_block(3)"), 8, 10)) == [[0], [1], [2]]
     empty_tail = P.csr_from_triplets(5, 5, [(0, 0, 1.0), (1, 1, 1.0)])
     assert rows(P.inspect(KernelKind.Spmv, empty_tail, 8, 2)) == [[0], [1, 2, 3, 4]]
     heavy = P.csr_from_triplets(4, 8, [(0, j, 1.0) for j in range(8)] + [(i, 0, 1.0) for i in range(1, 4)])
@@ -105,11 +105,11 @@ def test_scheduler_known_answers():
 def test_inspect_validates_arguments():
     """test_miner.cpp:254-258."""
     with pytest.raises(P.InvalidArgument):
-        P.inspect(KernelKind.Spmv, P.dense_block(2), 0, 1)
+        P.inspect(KernelKind.Spmv, pattern("dense_block(2)"), 0, 1)
     with pytest.raises(P.InvalidArgument):
-        P.inspect(KernelKind.Spmv, P.dense_block(2), 1, 0)
+        P.inspect(KernelKind.Spmv, pattern("dense_block(2)"), 1, 0)
     with pytest.raises(P.InvalidArgument):
-        P.inspect(KernelKind.Sptrsv, P.dense_block(2), 1, 1)
+        P.inspect(KernelKind.Sptrsv, pattern("dense_block(2)"), 1, 1)
 
 
 def test_every_plan_is_valid_and_minimal():
@@ -124,7 +124,7 @@ def test_every_plan_is_valid_and_minimal():
 
 
 def test_export_import_roundtrip_and_validate_plan_errors():
-    a = P.random_uniform(30, 30, 0.2, 17)
+    a = pattern("random_uniform(30,30,0.2,17)")
     plan = P.inspect(KernelKind.Spmv, a, 3, 4)
     counts, arrays, keep = plan.export_arrays()
     back = P.CodeletPlan.from_arrays(counts, arrays, keep)

@@ -10,7 +10,7 @@ import paper_2111_12243_b200 as P
 from oracle.oracle import Oracle, Ref
 from paper_2111_12243_b200 import KernelKind
 from paper_2111_12243_b200.psc import ExecutionContext, _codelet_view
-from tests.helpers import bitwise_equal, golden_cases, suite_cases, suite_input
+from tests.helpers import bitwise_equal, golden_cases, suite_cases, suite_input, pattern
 
 
 def _exec(which, c, ax, x, acc):
@@ -49,7 +49,7 @@ def test_known_answer_solves():
     plan = P.inspect(KernelKind.Sptrsv, l, 2, 1)
     x, _ = Oracle.run_sptrsv(plan.export_arrays(), l.view(), b)
     assert x.tolist() == [1, 1, 1.5]
-    a = P.dense_block(3)
+    a = pattern("dense_block(3)")
     plan = P.inspect(KernelKind.Spmv, a, 3, 1)
     assert Oracle.run_spmv(plan.export_arrays(), a.view(), np.ones(3)).tolist() == [6, 15, 24]
 
