@@ -1,19 +1,26 @@
 #!/usr/bin/env python
 """Benchmark of the DDF codelet executor on B200 (BASELINE.json metric:
-SpMV/SpTRSV fp64 GFLOP/s and % of the HBM roofline).
+SpMV/SpTRSV fp64 GFLOP/s and % of the HBM roofline at 1/2/4/8 B200 vs host CPU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--mode fast|parity]
+                    [--impl ours|reference]
 
-Default workload: BASELINE.json configs[1] -- SpTRSV on the lower triangle of
-the 3-D 7-point Laplacian, 100^3 grid (n = 1e6, nnz = 3.97e6), plan t=3,
-groups=8. A step is one complete triangular solve (one kernel launch). The
-solve does not shard, so N > 1 runs N independent replicas
-("scaling": "weak"). SpMV configs (--config 1/3/5) shard the plan's partitions
-across ranks with an NCCL all-gather of x per step ("scaling": "strong").
+Default workload: BASELINE.json configs[4] -- SpMV on the symmetric power-law
+matrix, n = 20M, nnz = 401M (the largest single-GPU configuration, and the one
+the 1/2/4/8-GPU metric is defined on), plan t=3, groups=8, fast mode
+(reassociated sums, gated at 1e-12 normwise against the reference's naive
+baseline); the parity mode (bitwise equal to the reference executor) is timed
+on the same workload and reported beside it. A step is one complete
+y = A x. With N > 1 the plan's partitions are sharded over the ranks (row
+shards, scheduler.cpp:67-89) and each step all-gathers x over NCCL first
+("scaling": "strong"); SpTRSV configs (2, 4) run N replicas ("weak").
+
+--gpus N without torchrun re-launches this script under
+torch.distributed.run with N ranks; under torchrun the world size must be N.
 
 Timing: W untimed warm-up steps; K timed steps between a barrier +
-cudaDeviceSynchronize on both sides; each step is bracketed by CUDA events
-on the launching stream with an L2 flush before it, outside the events (a
+cudaDeviceSynchronize on both sides; each step is bracketed by CUDA events on
+the launching stream with an L2 flush before it, outside the events (a
 2x-L2 write, then a 2x-L2 read of a second buffer, so no dirty flush lines are
 written back during the step); ms_per_step is the mean device time, maxed
 over ranks.
@@ -22,8 +29,8 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -41,6 +48,7 @@ CONFIGS = {
     4: ("sptrsv", "config4-sptrsv-supernodal-400k"),
     5: ("spmv", "config5-spmv-powerlaw-20M"),
 }
+METRIC = "fp64 GFLOP/s of the codelet executor (2*nnz SpMV / 2*nnz-n SpTRSV)"
 CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                 "clocks_event_reasons.sw_power_cap")
@@ -50,17 +58,17 @@ REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_powe
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
-    p.add_argument("--warmup", type=int, default=10)
-    p.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    p.add_argument("--mode", default="fast", choices=["fast", "parity"],
+                   help="SpMV summation: fast (reassociated, 1e-12 normwise) or parity (bitwise the reference's)")
     p.add_argument("--scale", type=float, default=1.0)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--t", type=int, default=3)
     p.add_argument("--groups", type=int, default=8)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=6.0, help="bounded CPU-baseline sample length")
-    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                   help="sharded SpMV x exchange: fused peer-memory pull (p2p) or NCCL all-gather")
+    p.add_argument("--cpu-repeats", type=int, default=3, help="reference run_bench repetitions (CPU baseline)")
     return p.parse_args()
 
 
@@ -69,8 +77,29 @@ def flops(kernel, n_rows, nnz):
     return 2 * nnz if kernel == "spmv" else 2 * nnz - n_rows
 
 
+def config_dict(args, kernel, workload, n, nnz, world):
+    """The same dict from both arms (the driver compares them)."""
+    sharded = kernel == "spmv" and world > 1
+    return {"workload": workload, "kernel": kernel, "n": n, "nnz": nnz, "t": args.t, "groups": args.groups,
+            "scale": args.scale, "mode": args.mode if kernel == "spmv" else "parity",
+            "parallelism": (f"row shards x{world} (x all-gather per step)" if sharded else
+                            (f"replicas x{world}" if world > 1 else "single device")),
+            "l2": "flushed before every timed step (2x-L2 write, then 2x-L2 read of a second buffer)"}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms."""
 
     def __init__(self, index):
         self.samples = []
@@ -78,7 +107,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(index), f"--query-gpu={CLOCK_FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -119,101 +148,125 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, mode):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(workload)
+            return json.load(f).get(f"{workload}/{mode}")
     except Exception:
         return None
 
 
-def cpu_baseline(kernel, a, plan_t, groups, vec, seconds):
-    """The reference executor (oracle/_ref) on the host cores; bounded sample."""
-    from oracle.oracle import Oracle, Ref
+def cpu_baseline(kernel, csr_view, args, vec, results):
+    """The reference's own run_bench (bench.cpp:118-187: inspect, then paired
+    medians of the naive baseline and the executor) on the host cores: SpMV
+    at every host thread and at 1 worker; SpTRSV at 1 worker (the reference
+    pool races on deep level-set solves). As the checker (not
+    timed), the reference executor and naive baseline also run once on the
+    bench's input and every GPU mode's result is compared with them."""
+    from oracle.oracle import Ref
 
-    n_flops = flops(kernel, a.n_rows, a.nnz())
-    kind = "reference" if Ref.available() else "port"
-    workers = 1 if kernel == "sptrsv" else (os.cpu_count() or 1)
-    if kind == "reference":
-        rc = Ref.csr(a.view())
-        rplan, _ = Ref.time_inspect(0 if kernel == "spmv" else 1, rc, plan_t, groups)
-        probe_fn = Ref.time_spmv if kernel == "spmv" else Ref.time_sptrsv
-        t1, _ = probe_fn(rplan, rc, vec, workers, 1, 1)
-        reps = int(max(3, min(1000, seconds / max(t1[0], 1e-6))))
-        times, _ = probe_fn(rplan, rc, vec, workers, 0, reps)
+    if not Ref.available():
+        return ({"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "unavailable",
+                 "sample": "oracle/_ref (the reference library) was not built"}, "unchecked (no reference library)")
+    rc = Ref.csr(csr_view)
+    k = 0 if kernel == "spmv" else 1
+    nproc = os.cpu_count() or 1
+    plan, insp = Ref.time_inspect(k, rc, args.t, args.groups)
+    n_flops = flops(kernel, csr_view.n_rows, csr_view.nnz)
+    runs = {}
+    for w in ([nproc, 1] if kernel == "spmv" else [1]):
+        runs[w] = Ref.paired_timing(plan, rc, k, vec, w, args.cpu_repeats if w > 1 else max(1, args.cpu_repeats - 1))
+    top = max(runs)
+    base_s = runs[top][0]
+    cpu = {"value": n_flops / runs[top][1] / 1e9, "unit": "GFLOP/s", "cores": top, "kind": "reference",
+           "sample": (f"the reference inspector once, then run_bench's paired protocol (bench.cpp:88-104: one "
+                      f"warm-up, {args.cpu_repeats} alternating repetitions, medians) of the naive CSR baseline and "
+                      f"psc::run_{kernel} on the full matrix at workers={top}"
+                      + (f" and at workers=1 ({max(1, args.cpu_repeats - 1)} repetitions)" if len(runs) > 1 else "")),
+           "cpu_model": cpu_model(),
+           "executor_ms": {str(w): r[1] * 1e3 for w, r in runs.items()},
+           "executor_gflops": {str(w): n_flops / r[1] / 1e9 for w, r in runs.items()},
+           "naive_baseline_ms": base_s * 1e3,
+           "naive_baseline_gflops": n_flops / base_s / 1e9,
+           "reference_inspector_s": insp}
+    # the checker: the reference executor and naive baseline on this input
+    if kernel == "spmv":
+        want, base = Ref.run_spmv(plan, rc, vec, nproc), Ref.spmv_baseline(rc, vec)
     else:
-        import paper_2111_12243_b200 as P
-
-        plan = P.inspect(P.KernelKind.Spmv if kernel == "spmv" else P.KernelKind.Sptrsv, a, plan_t, groups)
-        exp = plan.export_arrays()
-        fn = (lambda: Oracle.run_spmv(exp, a.view(), vec)) if kernel == "spmv" else \
-            (lambda: Oracle.run_sptrsv(exp, a.view(), vec))
-        times = []
-        t_end = time.time() + seconds
-        while len(times) < 3 or time.time() < t_end:
-            s = time.perf_counter()
-            fn()
-            times.append(time.perf_counter() - s)
-        workers = 1
-    med = float(np.median(times))
-    return {"value": n_flops / med / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": kind,
-            "sample": f"{len(times)} complete run_{kernel} calls on the full matrix (median {med * 1e3:.2f} ms), "
-                      f"plan t={plan_t} groups={groups}, workers={workers}"
-                      + (" (the reference pool races on deep level-set solves, SURVEY.md §0.8; with 4 or 16 workers it segfaults 3/3 on config 2, tools/ref_workers_probe.py)"
-                         if kernel == "sptrsv" and kind == "reference" else ""),
-            "ms_median": med * 1e3}
+        want, base = Ref.run_sptrsv(plan, rc, vec, 1)[0], Ref.sptrsv_baseline(rc, vec)
+    den = float(np.max(np.abs(base))) or 1.0
+    tol = 1e-12 if kernel == "spmv" else 1e-10
+    check = {"tolerance_normwise": tol}
+    for mode, got in results.items():
+        if mode is None or got is None:
+            continue
+        bitwise = bool(np.array_equal(got.view(np.int64), want.view(np.int64)))
+        nw = float(np.max(np.abs(got - base)) / den)
+        check[mode] = {"bitwise_vs_reference_executor": bitwise, "normwise_vs_reference_baseline": nw,
+                       "ok": bitwise if mode == "parity" else nw <= tol}
+    return cpu, check
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU executor on this box's host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's own CPU executor (oracle/_ref, built
+    from /root/reference) on this box's host cores, every host thread; the
+    inputs come from configs.cpp compiled into that same library, so no
+    product library is loaded."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    import paper_2111_12243_b200 as P
-    from oracle.oracle import Oracle, Ref
+    from oracle.oracle import Ref
 
     kernel, workload = CONFIGS[args.config]
-    a = P.generate_config(args.config, args.scale)
-    vec = P.uniform_vector(a.n_cols, 10 + args.config)
-    n_flops = flops(kernel, a.n_rows, a.nnz())
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpsc_ref.so was not built"}), flush=True)
+        return
+    a = Ref.generate_config(args.config, args.scale)
+    v = a.view()
+    vec = Ref.uniform_vector(v.n_cols, 10 + args.config)
+    n_flops = flops(kernel, v.n_rows, v.nnz)
     workers = 1 if kernel == "sptrsv" else (os.cpu_count() or 1)
-    if Ref.available():
-        kind = "reference"
-        rc = Ref.csr(a.view())
-        rplan, insp = Ref.time_inspect(0 if kernel == "spmv" else 1, rc, args.t, args.groups)
-        fn = Ref.time_spmv if kernel == "spmv" else Ref.time_sptrsv
-        times, _ = fn(rplan, rc, vec, workers, args.warmup, args.steps)
-    else:
-        kind, workers = "port", 1
-        t0 = time.perf_counter()
-        plan = P.inspect(P.KernelKind.Spmv if kernel == "spmv" else P.KernelKind.Sptrsv, a, args.t, args.groups)
-        insp = time.perf_counter() - t0
-        exp = plan.export_arrays()
-        run = (lambda: Oracle.run_spmv(exp, a.view(), vec)) if kernel == "spmv" else \
-            (lambda: Oracle.run_sptrsv(exp, a.view(), vec))
-        for _ in range(args.warmup):
-            run()
-        times = []
-        for _ in range(args.steps):
-            s = time.perf_counter()
-            run()
-            times.append(time.perf_counter() - s)
-    times = np.asarray(times)
+    rplan, insp = Ref.time_inspect(0 if kernel == "spmv" else 1, a, args.t, args.groups)
+    fn = Ref.time_spmv if kernel == "spmv" else Ref.time_sptrsv
+    times, _ = fn(rplan, a, vec, workers, args.warmup, args.steps)
     value = n_flops * len(times) / times.sum() / 1e9
     line = {
-        "metric": "fp64 GFLOP/s of the codelet executor (2*nnz SpMV / 2*nnz-n SpTRSV)",
-        "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus, "device": "host CPU", "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(times.mean() * 1e3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE.json config generator)",
-        "impl": "reference",
-        "config": {"workload": workload, "n": a.n_rows, "nnz": a.nnz(), "t": args.t, "groups": args.groups,
-                   "kernel": kernel, "parallelism": f"cpu workers={workers}"},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": workers, "kind": kind,
-                         "sample": f"{len(times)} complete run_{kernel} calls on the full matrix"},
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(times.mean() * 1e3), "higher_is_better": True,
+        "scaling": "strong" if kernel == "spmv" and world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE.json config generator, DESIGN.md Inputs)", "impl": "reference",
+        "config": config_dict(args, kernel, workload, v.n_rows, v.nnz, world),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": workers, "kind": "reference",
+                         "sample": f"{len(times)} complete psc::run_{kernel} calls on the full matrix, "
+                                   f"workers={workers}, after {args.warmup} untimed ones",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_median": float(np.median(times) * 1e3),
         "inspector_seconds": insp,
+        "device": "host CPU",
+        "native_libs": mapped_repo_libs(),
     }
     print(json.dumps(line), flush=True)
+
+
+def mapped_repo_libs():
+    """This repo's shared libraries mapped into this process (the reference arm must map only oracle/_ref)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {line.split()[-1] for line in f if line.rstrip().endswith(".so")}
+        return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT))
+    except Exception:
+        return None
+
+
+def spawn(args):
+    """--gpus N without torchrun: re-launch under torch.distributed.run with N ranks."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def run_ours(args):
@@ -224,6 +277,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -232,13 +287,13 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     kernel, workload = CONFIGS[args.config]
+    mode = args.mode if kernel == "spmv" else "parity"
     kk = P.KernelKind.Spmv if kernel == "spmv" else P.KernelKind.Sptrsv
     a = P.generate_config(args.config, args.scale)
     t0 = time.perf_counter()
     plan = P.inspect(kk, a, args.t, args.groups)
     inspector_s = time.perf_counter() - t0
-    # the same inspection with the window mining on the GPU (same plan, bit for bit)
-    t0 = time.perf_counter()
+    t0 = time.perf_counter()  # the same inspection with the window mining on the GPU (same plan, bit for bit)
     plan_dev = P.inspect_device(kk, a, args.t, args.groups, local)
     inspector_dev_s = time.perf_counter() - t0
     inspector_dev_same = plan_dev.hash() == plan.hash()
@@ -246,11 +301,13 @@ def run_ours(args):
     exe = P.Executor(1, local)
     n_parts = plan.counts().n_partitions
     sharded = kernel == "spmv" and world > 1
+    parts = None
     if sharded:
-        p0, p1 = rank * n_parts // world, (rank + 1) * n_parts // world
-        bound = P.BoundPlan(exe, plan, a, partitions=(p0, p1))
-    else:
-        bound = P.BoundPlan(exe, plan, a)
+        from paper_2111_12243_b200.dist import shard_partitions
+
+        parts = shard_partitions(n_parts, world, rank)
+    mode_id = 1 if mode == "fast" else 0
+    bound = P.BoundPlan(exe, plan, a, mode=mode_id, partitions=parts)
     info = bound.info()
     dev = torch.device("cuda", local)
     vec_h = P.uniform_vector(a.n_cols, 10 + args.config)
@@ -259,91 +316,27 @@ def run_ours(args):
     out = torch.empty(max(rows, 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
-    exchange_kind = None
-    peer_ex = None
-    if sharded and args.exchange == "p2p":
-        # fused exchange: one launch pulls the shard's remote columns from the
-        # peers' IPC windows over NVLink and multiplies (dist.PeerExchange)
-        from paper_2111_12243_b200.dist import PeerExchange, shard_row_ranges
+    if sharded:
+        # every rank owns the x slice of its rows; a step all-gathers x (NCCL), then multiplies
+        from paper_2111_12243_b200.dist import XExchange, shard_row_ranges
 
-        try:
-            bound.x_runs()  # raises for shards the fused path does not take (segmented plans)
-            peer_ex = PeerExchange(bound, shard_row_ranges(plan, world), rank, a.n_cols)
-        except Exception as e:  # e.g. a segmented plan or no peer access: fall back to NCCL
-            exchange_kind = f"nccl (p2p unavailable: {type(e).__name__}: {e})"
-            peer_ex = None
-        flag = torch.tensor([1 if peer_ex is not None else 0], device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if flag.item() == 0 and peer_ex is not None:
-            peer_ex.close()
-            peer_ex = None
-            exchange_kind = exchange_kind or "nccl (p2p unavailable on a peer)"
-    if peer_ex is not None:
-        exchange_kind = "p2p (fused peer-memory pull + multiply)"
+        xex = XExchange(shard_row_ranges(plan, world), a.n_cols, dev)
         x_mine = vec[bound.row_begin:bound.row_end].clone()
 
-        def step(ev_mid=None):
-            if ev_mid is not None:
-                ev_mid.record()
-            peer_ex.multiply(x_mine, out)
-    elif sharded:
-        exchange_kind = exchange_kind or "nccl all-gather"
-        # every rank owns the x slice of its rows; a step all-gathers x then multiplies
-        sizes = torch.tensor([rows], device=dev)
-        all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
-        dist.all_gather(all_sizes, sizes)
-        sizes_l = [int(s.item()) for s in all_sizes]
-        pad = max(sizes_l)
-        x_local = torch.zeros(pad, dtype=torch.float64, device=dev)
-        x_local[:rows] = vec[bound.row_begin:bound.row_end]
-        x_gathered = torch.empty(pad * world, dtype=torch.float64, device=dev)
-        x_full = torch.empty(a.n_cols, dtype=torch.float64, device=dev)
-        offs = np.concatenate([[0], np.cumsum(sizes_l)])
-
-        def exchange():
-            dist.all_gather_into_tensor(x_gathered, x_local)
-            for r in range(world):
-                x_full[offs[r]:offs[r + 1]] = x_gathered[r * pad:r * pad + sizes_l[r]]
-
-        def step(ev_mid=None):
-            exchange()
-            if ev_mid is not None:
-                ev_mid.record()
-            bound.spmv(x_full, out)
+        def step(b=bound):
+            b.spmv(xex.exchange(x_mine), out)
     elif kernel == "spmv":
-        def step(ev_mid=None):
-            if ev_mid is not None:
-                ev_mid.record()
-            bound.spmv(vec, out)
+        def step(b=bound):
+            b.spmv(vec, out)
     else:
-        def step(ev_mid=None):
-            if ev_mid is not None:
-                ev_mid.record()
-            bound.sptrsv(vec, out)
+        def step(b=bound):
+            b.sptrsv(vec, out)
 
-    # ---- parity against the C oracle, once, before timing ----
-    parity = "unchecked"
-    got = None
-    try:
-        from oracle.oracle import Oracle
-
-        step()
-        torch.cuda.synchronize()
-        got = out[:rows].cpu().numpy()
-        exp = plan.export_arrays()
-        if kernel == "spmv":
-            want = Oracle.run_spmv(exp, a.view(), vec_h)[bound.row_begin:bound.row_end]
-        else:
-            want = Oracle.run_sptrsv(exp, a.view(), vec_h)[0]
-        parity = "bitwise" if np.array_equal(got.view(np.int64), want.view(np.int64)) else "MISMATCH"
-        del exp
-    except Exception as e:  # the oracle is a checker only; a failure here is reported, not hidden
-        parity = f"unchecked ({type(e).__name__}: {e})"
+    step()
+    torch.cuda.synchronize()
+    got = out[:rows].cpu().numpy()
 
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    # L2 flush between steps: write a 2x-L2 buffer, then read a second one, so
-    # the step starts cold AND without dirty flush lines (their write-back
-    # would otherwise be charged to the step's own HBM traffic)
     flush_buf = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
     clean_buf = torch.ones(2 * l2 // 4, dtype=torch.float32, device=dev)
     clean_sink = torch.empty((), dtype=torch.float32, device=dev)
@@ -351,31 +344,47 @@ def run_ours(args):
     def flush():
         flush_buf.zero_()
         torch.sum(clean_buf, 0, out=clean_sink)
+
+    def timed(fn, steps, warmup, barrier):
+        for _ in range(warmup):
+            flush()
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if barrier and dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.time()
+        for i in range(steps):
+            flush()
+            ev[i][0].record()
+            fn()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        if barrier and dist:
+            dist.barrier()
+        w1 = time.time()
+        return np.array([s.elapsed_time(e) for s, e in ev]), w0, w1
+
     sampler = ClockSampler(local)
+    step_ms, wall0, wall1 = timed(step, args.steps, args.warmup, True)
 
-    for _ in range(args.warmup):
-        flush()
-        step()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    wall0 = time.time()
-    for i in range(args.steps):
-        flush()
-        ev[i][0].record()
-        step(ev[i][1])
-        ev[i][2].record()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    wall1 = time.time()
-    step_ms = np.array([s.elapsed_time(e) for s, _, e in ev])
-    kern_ms = np.array([m.elapsed_time(e) for _, m, e in ev])
+    # ---- the other SpMV mode on the same workload (parity when the headline is fast) ----
+    other, other_got = None, None
+    if kernel == "spmv" and not sharded:
+        other_mode = "parity" if mode == "fast" else "fast"
+        ob = P.BoundPlan(exe, plan, a, mode=1 if other_mode == "fast" else 0)
+        ob.spmv(vec, out)
+        torch.cuda.synchronize()
+        other_got = out[:rows].cpu().numpy()
+        oms, _, _ = timed(lambda: ob.spmv(vec, out), max(3, args.steps // 5), 2, False)
+        other = {"mode": other_mode, "ms_per_step": float(oms.mean()),
+                 "value": flops(kernel, a.n_rows, a.nnz()) / (oms.mean() * 1e-3) / 1e9,
+                 "frac_of_hbm_peak": info["algorithmic_bytes"] / (oms.mean() * 1e-3) / 1e9 / measured_peak()[0],
+                 "launches_per_step": ob.launches()}
+        ob.close()
 
-    # ---- e2e: host buffers through the C ABI (H2D input, kernel, D2H result) ----
-    e2e_parity = "unchecked"
+    # ---- e2e: the public host-buffer API (H2D input, kernels, D2H result) ----
+    e2e_check = None
     if sharded:
         e2e_ms = step_ms.copy()  # x already device-resident per rank; reported as the exchange+compute step
         h2d = d2h = 0
@@ -383,50 +392,46 @@ def run_ours(args):
         host_in = torch.from_numpy(vec_h.copy()).pin_memory()
         host_out = torch.empty(max(rows, 1), dtype=torch.float64).pin_memory()
         hin, hout = host_in.numpy(), host_out.numpy()
+        call = bound.spmv_host if kernel == "spmv" else bound.sptrsv_host
         for _ in range(max(1, args.warmup)):
-            (bound.spmv_host if kernel == "spmv" else bound.sptrsv_host)(hin, hout, stream=stream)
+            call(hin, hout, stream=stream)
         torch.cuda.synchronize()
         e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(args.steps)]
         for i in range(args.steps):
             e2e_ev[i][0].record()
-            (bound.spmv_host if kernel == "spmv" else bound.sptrsv_host)(hin, hout, stream=stream)
+            call(hin, hout, stream=stream)
             e2e_ev[i][1].record()
         torch.cuda.synchronize()
         e2e_ms = np.array([s.elapsed_time(e) for s, e in e2e_ev])
         h2d, d2h = 8 * a.n_cols, 8 * rows
-        if got is not None and rows > 0:  # the host-buffer result against the device path's (oracle-checked) one
-            e2e_parity = ("bitwise (equal to the device path)"
-                          if np.array_equal(hout[:rows].view(np.int64), got.view(np.int64)) else "MISMATCH")
+        e2e_check = "bitwise equal to the device path" if np.array_equal(hout[:rows].view(np.int64), got.view(np.int64)) \
+            else "MISMATCH"
     sampler.stop()
 
-    ms_step = float(step_ms.mean())
-    ms_kern = float(kern_ms.mean())
-    ms_e2e = float(e2e_ms.mean())
+    ms_step, ms_e2e = float(step_ms.mean()), float(e2e_ms.mean())
     if dist:
-        t = torch.tensor([ms_step, ms_kern, ms_e2e], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_step, ms_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, ms_kern, ms_e2e = [float(v) for v in t.tolist()]
+        ms_step, ms_e2e = [float(v) for v in t.tolist()]
     total_flops = flops(kernel, a.n_rows, a.nnz())
     units = total_flops if sharded else total_flops * world  # replicas: every rank does the whole job
     value = units / (ms_step * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    achieved = info["algorithmic_bytes"] / (ms_kern * 1e-3) / 1e9
-    traffic = ncu_traffic(workload)
+    achieved = info["algorithmic_bytes"] / (ms_step * 1e-3) / 1e9
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    cpu = None
+    cpu, parity = None, "unchecked (N > 1, or --no-cpu-baseline)"
     if not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_baseline(kernel, a, args.t, args.groups, vec_h, args.cpu_seconds)
-        except Exception as e:
-            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "unavailable",
-                   "sample": f"{type(e).__name__}: {e}"}
-    clocks = sampler.summary(wall0, wall1)
+            cpu, parity = cpu_baseline(kernel, a.view(), args, vec_h, {mode: got, other["mode"] if other else None: other_got})
+        except Exception as e:  # reported, not hidden
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "unavailable", "sample": f"{type(e).__name__}: {e}"}
+            parity = f"unchecked ({type(e).__name__}: {e})"
     line = {
-        "metric": "fp64 GFLOP/s of the codelet executor (2*nnz SpMV / 2*nnz-n SpTRSV)",
+        "metric": METRIC,
         "value": value,
         "unit": "GFLOP/s",
         "n_gpus": world,
@@ -438,35 +443,39 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json config generator, DESIGN.md Inputs)",
-        "config": {
-            "workload": workload, "kernel": kernel, "n": a.n_rows, "nnz": a.nnz(), "t": args.t,
-            "groups": args.groups, "partitions": n_parts, "scale": args.scale,
-            "parallelism": (f"row-sharded x{world} (x exchange: {exchange_kind})" if sharded else
-                            (f"replicas x{world}" if world > 1 else "single GPU")),
-            "l2": "flushed before every timed step, outside the events: 2x-L2 write, then 2x-L2 read of a second buffer (cold, no dirty lines)",
-            "mode": "parity (bitwise equal to the reference executor)",
-            "bound": info,
-        },
+        "config": config_dict(args, kernel, workload, a.n_rows, a.nnz(), world),
         "parity": parity,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": info["algorithmic_bytes"], "kernel_ms": ms_kern,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(workload, mode),
+                     "algorithmic_bytes_per_step": info["algorithmic_bytes"],
+                     "bytes_formula": ("12*nnz + 4*(n+1) + 8*n_cols + 8*n (SpMV)" if kernel == "spmv" else
+                                       "12*nnz + 4*(n+1) + 16*n (SpTRSV)") + ", SURVEY.md §8d",
+                     "timed": f"the whole step ({bound.launches()} launches of this repo's kernels) per CUDA events on the launching stream",
                      "peak_source": peak_src, "frac_of_nominal_8TBps": achieved / 8000.0},
+        "other_mode": other,
         "cpu_baseline": cpu,
         "e2e": {"value": total_flops * (1 if sharded else world) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                "path": "psc_bound_*_host (pinned host buffers; SpTRSV: b gathered from mapped host memory unit by unit in level order during the solve, x shipped per finished unit by bulk copies; column-split SpMV: x uploaded range by range ahead of its pass, y sent down per row slice of the last pass)",
-                "parity": e2e_parity},
+                "path": "psc_bound_*_host with pinned host buffers (the C ABI's host-buffer entry points)",
+                "check": e2e_check},
         "gpu_launches": args.steps * bound.launches(),
-        "clocks": clocks,
+        "clocks": sampler.summary(wall0, wall1),
         "inspector_seconds": inspector_s,
         "inspector_device_seconds": inspector_dev_s,
         "inspector_device_plan_equal": inspector_dev_same,
+        "bound": info,
     }
-    if kernel == "sptrsv":  # the solve is bound by its dependency chain, not by HBM
+    if kernel == "sptrsv":  # the solve is bound by its dependency chain
         line["roofline"]["critical_path"] = {
-            "levels": n_parts, "ns_per_level": ms_kern * 1e6 / max(1, n_parts),
-            "note": "sync-free solve: time ~ levels x per-level hop latency; HBM frac is not the binding limit"}
+            "levels": n_parts, "ns_per_level": ms_step * 1e6 / max(1, n_parts),
+            "note": "sync-free solve: time ~ levels x per-level hop latency"}
+        line["roofline"]["record_pack"] = "the per-row record pack (trsv_pack_kernel) runs at bind and after a value change, outside the timed step"
+    if kernel == "spmv" and mode == "fast":
+        line["roofline"]["gather_bound"] = {
+            "note": "each entry gathers one x value at a random column (config 5); the L1/L2 path serves ~1 such gather "
+                    "per SM-cycle (tools/gather_probe.cu on this B200: 255 G gathers/s beside a 12 B/entry stream), "
+                    "so 401M gathers take >= ~1.57 ms whatever the HBM bandwidth (DESIGN.md)",
+            "gathers_per_step": a.nnz()}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -476,9 +485,12 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

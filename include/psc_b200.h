@@ -182,7 +182,10 @@ PSC_API void psc_executor_destroy(psc_executor* exec);
 /* Bind a plan and its matrix: lowers the plan to device segments and uploads
  * CSR + plan once (inspector-executor amortisation). The matrix view points to
  * HOST memory. mode: 0 = parity (bitwise equal to the reference executor),
- * 1 = fast (normwise-equal; FMA and tree reductions allowed). */
+ * 1 = fast: SpMV plans whose rows are single codelet rows (configs 1, 5) run
+ * with reassociated row sums (spmv_fast.cu; deterministic, within 1e-12
+ * normwise of the reference); other plans and SpTRSV run the parity kernels
+ * in either mode. */
 enum { PSC_MODE_PARITY = 0, PSC_MODE_FAST = 1 };
 PSC_API psc_status psc_bind(psc_executor* exec, const psc_plan* plan, const psc_csr_view* a,
                             int32_t mode, psc_bound** out);
@@ -214,8 +217,9 @@ PSC_API int64_t psc_bound_trace(const psc_bound* b, uint64_t* out, int64_t cap);
 PSC_API int32_t psc_bound_launches(const psc_bound* b);
 /* Lowering diagnostics, out[0..7]: rows, segments (0 = every row is one
  * implicit full-row segment), work units (SpMV chunks / SpTRSV row blocks),
- * path (0 parity-segments, 1 general interpreter), algorithmic bytes per call
- * (DESIGN.md), device bytes held, long rows, reserved. */
+ * path (0 parity kernels, 1 general interpreter, 2 fast-mode SpMV),
+ * algorithmic bytes per call, device bytes held, long rows,
+ * column passes (SpMV; 0 = one pass over all of x) / max block rows (SpTRSV). */
 PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]);
 /* ---- multi-GPU SpMV: fused x exchange over peer memory --------------------
  * A rank that bound a shard (psc_bind_partitions) of a simple SpMV plan reads

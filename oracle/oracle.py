@@ -229,6 +229,9 @@ class Ref:
             lib.ref_time_sptrsv.argtypes = [c_void_p, c_void_p, POINTER(c_double), POINTER(c_double),
                                             POINTER(c_double), c_int, c_int, c_int, POINTER(c_double)]
             lib.ref_time_inspect.argtypes = [c_int, c_void_p, c_int, c_int, POINTER(c_double), vp]
+            lib.ref_paired_timing.argtypes = [c_void_p, c_void_p, c_int, POINTER(c_double), c_int, c_int,
+                                              POINTER(c_double)]
+            lib.ref_run_bench.argtypes = [c_int, c_void_p, c_int, c_int, c_int, c_int, c_uint64, POINTER(c_double)]
             cls._lib = lib
         return cls._lib
 
@@ -366,6 +369,21 @@ class Ref:
         cls._check(cls.lib().ref_time_sptrsv(plan.h, l.h, _dp(b), _dp(x), _dp(acc), workers, warmup, reps,
                                              _dp(t)))
         return t, x
+
+    @classmethod
+    def run_bench(cls, kernel, a: RefCsr, t, groups, workers, repeats, seed=42) -> dict:
+        """psc::run_bench (bench.cpp:118-187): the reference's own paired-median measurement."""
+        out = (c_double * 6)()
+        cls._check(cls.lib().ref_run_bench(kernel, a.h, t, groups, workers, repeats, seed, out))
+        keys = ["inspector_seconds", "baseline_seconds", "executor_seconds", "gflops", "max_rel_error", "ner"]
+        return dict(zip(keys, [float(v) for v in out]))
+
+    @classmethod
+    def paired_timing(cls, plan: RefPlan, a: RefCsr, kernel: int, vec, workers: int, repeats: int):
+        """(baseline, executor) median seconds, bench.cpp:88-104 over an existing plan."""
+        out = (c_double * 2)()
+        cls._check(cls.lib().ref_paired_timing(plan.h, a.h, kernel, _dp(vec), workers, repeats, out))
+        return float(out[0]), float(out[1])
 
     @classmethod
     def time_inspect(cls, kernel, a, t, groups):

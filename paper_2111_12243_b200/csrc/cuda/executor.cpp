@@ -260,9 +260,11 @@ void build_split(psc_bound* b, const psc_csr_view& a, int parts, cudaStream_t s)
                 const int64_t t = static_cast<int64_t>(n) * i / psc_bound::kYSlices;
                 int ia = 0;
                 while (ia < n_it && items[4 * static_cast<size_t>(ia)] < t) ++ia;
-                const int32_t cut = i == psc_bound::kYSlices ? n : ia < n_it ? items[4 * static_cast<size_t>(ia)] : n;
+                // slice 0 starts at row 0 (rows before the first chunk are long rows), the
+                // last ends at n; the others start at a chunk's first row
+                const int32_t cut = i == 0 ? 0 : i == psc_bound::kYSlices ? n : ia < n_it ? items[4 * static_cast<size_t>(ia)] : n;
                 b->ysl_row[i] = cut;
-                b->ysl_item[i] = i == psc_bound::kYSlices ? n_it : ia;
+                b->ysl_item[i] = i == 0 ? 0 : i == psc_bound::kYSlices ? n_it : ia;
                 b->ysl_long[i] = static_cast<int>(std::lower_bound(longs.begin(), longs.end(), cut) - longs.begin());
             }
         }
@@ -1179,11 +1181,11 @@ PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]) {
         out[0] = b->rows();
         out[1] = b->canonical ? b->n_segments : -1;
         out[2] = b->kernel == PSC_KERNEL_SPMV ? b->n_chunks : b->n_blocks;
-        out[3] = b->canonical ? 0 : 1;
+        out[3] = !b->canonical ? 1 : b->fast_passes ? 2 : 0;
         out[4] = b->algorithmic_bytes();
         out[5] = b->device_bytes();
         out[6] = b->long_rows;
-        out[7] = b->max_block_rows;
+        out[7] = b->kernel == PSC_KERNEL_SPMV ? std::max(b->fast_passes, b->split) : b->max_block_rows;
     });
 }
 

@@ -806,8 +806,8 @@ class BoundPlan:
     def info(self) -> dict:
         out = (C.c_int64 * 8)()
         _check(_capi.lib().psc_bound_info(self._h, out))
-        keys = ["rows", "segments", "work_units", "general_path", "algorithmic_bytes", "device_bytes", "long_rows",
-                "max_block_rows"]
+        keys = ["rows", "segments", "work_units", "path", "algorithmic_bytes", "device_bytes", "long_rows",
+                "passes_or_block_rows"]
         return dict(zip(keys, [int(v) for v in out]))
 
     def close(self):

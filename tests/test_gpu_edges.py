@@ -248,6 +248,41 @@ def test_spmv_column_split(monkeypatch, force, parts):
     assert bound.launches() >= (2 if force else 1)
 
 
+@pytest.mark.parametrize("layout", ["first_row_long", "all_rows_long", "long_head_short_tail"])
+def test_spmv_column_split_host_slices(monkeypatch, layout):
+    """The host-buffer path runs the last column pass in row slices and sends
+    each slice's y down as it finishes: rows before the first chunk (long rows
+    in the last pass) and a last pass with only long rows must be covered too
+    (slice 0 started at the first chunk's row)."""
+    import torch
+
+    monkeypatch.setenv("PSC_SPMV_SPLIT_BYTES", "1")
+    monkeypatch.setenv("PSC_SPMV_SPLIT_PARTS", "2")
+    exe = P.Executor(1)
+    rng = np.random.default_rng(7)
+    n = 1200
+    long_rows = {"first_row_long": {0}, "all_rows_long": set(range(0, n, 150)),
+                 "long_head_short_tail": set(range(5))}[layout]
+    ent = []
+    for r in range(n if layout != "all_rows_long" else 8):
+        rr = r if layout != "all_rows_long" else r * 150
+        if rr in long_rows:
+            cols = np.arange(n // 2, n // 2 + 300)  # > 256 entries in the last (upper) column half
+            cols = np.concatenate([np.arange(0, 20), cols])
+        else:
+            cols = rng.choice(n, size=int(rng.integers(1, 6)), replace=False)
+        ent += [(rr, int(c), float(rng.uniform(-1, 1))) for c in cols]
+    a = _csr(n, n, ent)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(n, 9)
+    want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+    bound = P.BoundPlan(exe, plan, a)
+    for host in (np.full(n, np.nan), torch.full((n,), float("nan"), dtype=torch.float64).pin_memory().numpy()):
+        bound.spmv_host(x, host)
+        torch.cuda.synchronize()
+        assert bitwise_equal(host, want), layout
+
+
 def test_spmv_side_stream_concurrent_threads(monkeypatch):
     """Plans that fork work onto the side stream (row groups beside chunks,
     long rows beside chunks, column-split passes) driven from five host

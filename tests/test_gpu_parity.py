@@ -74,6 +74,41 @@ def test_configs_bitwise(exe, config, scale, kernel):
     assert normwise_err(got, baseline(kernel, a, vec)) <= tol
 
 
+@pytest.mark.parametrize("config,kernel", [(3, KernelKind.Spmv), (4, KernelKind.Sptrsv), (5, KernelKind.Spmv)])
+def test_configs_full_size_bitwise(exe, config, kernel):
+    """acceptance_main.cpp:127-174 criterion 1 at BASELINE.json's full sizes,
+    where the production paths engage: config 3's row groups and quad chunks,
+    config 4's streaming long-row solve, config 5's column-split passes (x =
+    160 MB) and long rows -- through the host-span API (run_spmv /
+    run_sptrsv) and, for the SpMV configs, the bound device and host-buffer
+    paths."""
+    import torch
+
+    a = P.generate_config(config, 1.0)
+    plan = P.inspect(kernel, a, 3, 8)
+    vec = P.uniform_vector(a.n_cols, 10 + config)
+    want = run_oracle(plan, kernel, a, vec)
+    got = run_gpu(exe, plan, kernel, a, vec)
+    assert bitwise_equal(got, want)
+    tol = 1e-12 if kernel == KernelKind.Spmv else 1e-10
+    assert normwise_err(got, baseline(kernel, a, vec)) <= tol
+    if kernel == KernelKind.Spmv:
+        bound = P.BoundPlan(exe, plan, a)
+        if config == 5:
+            assert bound.info()["passes_or_block_rows"] >= 2  # column-split passes engaged
+        xd = torch.from_numpy(vec).cuda()
+        yd = torch.full((a.n_rows,), float("nan"), dtype=torch.float64, device="cuda")
+        bound.spmv(xd, yd)
+        torch.cuda.synchronize()
+        assert bitwise_equal(yd.cpu().numpy(), want)
+        xp = torch.from_numpy(vec).pin_memory()
+        yp = torch.full((a.n_rows,), float("nan"), dtype=torch.float64).pin_memory()
+        bound.spmv_host(xp.numpy(), yp.numpy())
+        torch.cuda.synchronize()
+        assert bitwise_equal(yp.numpy(), want)
+        bound.close()
+
+
 def test_bound_device_path_matches_host_path(exe):
     import torch
 
