@@ -278,6 +278,15 @@ PSC_API psc_status psc_run_sptrsv(psc_executor* exec, const psc_plan* plan,
 PSC_API psc_status psc_execute_plan(psc_executor* exec, const psc_plan* plan, const psc_csr_view* a,
                                     const psc_exec_context* ctx);
 
+/* Executor::run (executor.hpp:45, executor.cpp:261-267) on a plan that
+ * carries its tables -- the reference's own CodeletPlan imported with
+ * psc_plan_from_arrays -- over a raw host context, no matrix argument:
+ * partitions in order, each group's codelets then its finalize records,
+ * accumulating onto ctx->accum (execute_plan(plan, ctx, workers) is a
+ * temporary executor's run). A plan mined by psc_inspect keeps its tables
+ * in the matrix: PSC_ERR_INVALID_ARGUMENT (use psc_execute_plan). */
+PSC_API psc_status psc_executor_run(psc_executor* exec, const psc_plan* plan, const psc_exec_context* ctx);
+
 /* Single-codelet execution on the GPU with exact exec_*_codelet semantics
  * (executor.cpp:53-116), including hand-built codelets with arbitrary tables.
  * Pointers are HOST memory laid out as in ExecutionContext (executor.hpp:17-23);

@@ -5,7 +5,8 @@
 //   psc::Executor exec(workers);                       psc_b200::Executor exec(workers);
 //   psc::run_spmv(plan, a, x, y, exec);                psc_b200::run_spmv(plan, a, x, y, exec);
 //   psc::run_sptrsv(plan, l, b, x, acc, exec);         psc_b200::run_sptrsv(plan, l, b, x, acc, exec);
-//   psc::execute_plan(plan, ctx, workers);             psc_b200::execute_plan(plan, a, ctx, workers);
+//   exec.run(plan, ctx);                               exec.run(plan, ctx);
+//   psc::execute_plan(plan, ctx, workers);             psc_b200::execute_plan(plan, ctx, workers);
 //   psc::exec_{blas,psci,pscii}_codelet(c, ctx);       psc_b200::exec_*_codelet(c, ctx);
 //
 // `plan` may be the reference's own psc::CodeletPlan (miner.hpp:73-89) -- it is
@@ -153,6 +154,16 @@ class Executor {
     int workers() const { return psc_executor_workers(e_.get()); }
     psc_executor* handle() const { return e_.get(); }
 
+    // Executor::run (executor.hpp:45): the plan over a raw ExecutionContext,
+    // accumulating onto ctx.accum. The plan must carry its tables (the
+    // reference's CodeletPlan); plans mined by this library's inspector keep
+    // them in the matrix -- use execute_plan(plan, a, ctx, workers).
+    template <class P, class Ctx>
+    void run(const P& plan, const Ctx& ctx) {
+        psc_exec_context c{ctx.matrix_values, ctx.gather, ctx.accum, ctx.rhs, ctx.solution};
+        check(psc_executor_run(e_.get(), plan_for(plan).handle(), &c));
+    }
+
     // Library plan for `plan`: itself, or the cached import of a reference plan.
     template <class P>
     const Plan& plan_for(const P& plan) {
@@ -197,8 +208,16 @@ void run_sptrsv(const P& plan, const L& l, std::span<const double> b, std::span<
                          x.data(), static_cast<int64_t>(x.size()), acc.data(), static_cast<int64_t>(acc.size())));
 }
 
-// execute_plan, executor.cpp:269-272 (the matrix supplies the CSR structure
-// of the plan; values come from ctx.matrix_values)
+// execute_plan, executor.cpp:269-272 (executor.hpp:54): a temporary
+// executor's run over a raw context
+template <class P, class Ctx>
+void execute_plan(const P& plan, const Ctx& ctx, int workers) {
+    Executor exec(workers);
+    exec.run(plan, ctx);
+}
+
+// The same for plans mined by this library (implicit tables): the matrix
+// supplies the CSR structure; values come from ctx.matrix_values
 template <class P, class M, class Ctx>
 void execute_plan(const P& plan, const M& a, const Ctx& ctx, int workers) {
     Executor exec(workers);

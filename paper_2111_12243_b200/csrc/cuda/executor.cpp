@@ -425,7 +425,8 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 // (config 5, x = 160 MB: 2 / 3 / 4 ranges 2.27 / 2.05 / 2.31 ms; one range 4.9 ms)
                 const int64_t part_bytes = v ? std::atoll(v) : 55000000LL;
                 const int64_t xb = static_cast<int64_t>(a.n_cols) * 8;
-                int parts = part_bytes > 0 && xb > 100000000LL ? static_cast<int>((xb + part_bytes - 1) / part_bytes) : 1;
+                // (by default only once x outgrows ~100 MB of the L2; a set PSC_FAST_SPLIT_BYTES always applies)
+                int parts = part_bytes > 0 && (v || xb > 100000000LL) ? static_cast<int>((xb + part_bytes - 1) / part_bytes) : 1;
                 parts = std::max(1, std::min(kMaxSplitPasses, parts));
                 build_fast(b.get(), a, ro, parts, s);
             } else if (allow_split && L.simple && L.row_begin == 0 && L.row_end == a.n_rows) {
@@ -1284,50 +1285,93 @@ PSC_API psc_status psc_execute_plan(psc_executor* e, const psc_plan* plan, const
 
 namespace {
 
+// Runs a general-path lowering over a raw host context with exact
+// Executor::run semantics (executor.cpp:261-267): partitions in order, each
+// group's codelets then its finalize records; accumulates onto ctx->accum,
+// writes ctx->solution at the finalized rows. Only the index ranges the
+// descriptors and finalize records touch are moved; a gather aliasing the
+// solution (the solve, executor.hpp:12-16) is one device buffer.
+void run_lowered_on_host_context(const Lowered& L, const psc_exec_context* ctx, const char* who) {
+    const auto& G = L.gen;
+    int n = psc_device_count();
+    if (n <= 0) throw CudaError(std::string(who) + ": no CUDA device is available");
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    psc_bound b;
+    b.device = dev;
+    b.canonical = false;
+    cudaStream_t s = nullptr;
+    b.part_group_ptr = G.part_group_ptr;
+    b.g_cp.upload(G.group_codelet_ptr, s);
+    b.g_fp.upload(G.group_fin_ptr, s);
+    b.g_kind.upload(G.c_kind, s);
+    b.g_m.upload(G.c_m, s);
+    b.g_n.upload(G.c_n, s);
+    b.g_form.upload(G.d_form, s);
+    b.g_base.upload(G.d_base, s);
+    b.g_so.upload(G.d_so, s);
+    b.g_si.upload(G.d_si, s);
+    b.g_tab.upload(G.d_tab, s);
+    b.g_tables.upload(G.tables, s);
+    b.g_frow.upload(G.f_row, s);
+    b.g_fdiag.upload(G.f_diag, s);
+    b.g_frhs.upload(G.f_rhs, s);
+    int64_t max_frow = -1, max_fdiag = -1, max_frhs = -1;
+    for (size_t f = 0; f < G.f_row.size(); ++f) {
+        max_frow = std::max<int64_t>(max_frow, G.f_row[f]);
+        max_fdiag = std::max<int64_t>(max_fdiag, G.f_diag[f]);
+        max_frhs = std::max<int64_t>(max_frhs, G.f_rhs[f]);
+    }
+    const bool finalize = max_frow >= 0;
+    const int64_t nm = std::max(G.max_mat, max_fdiag) + 1, nv = G.max_vec + 1,
+                  no = std::max(G.max_out, max_frow) + 1, ns = max_frow + 1, nr = max_frhs + 1;
+    const std::string w(who);
+    if (nm > 0) require(ctx->matrix_values != nullptr, w + ": null matrix_values");
+    if (nv > 0) require(ctx->gather != nullptr, w + ": null gather");
+    if (no > 0) require(ctx->accum != nullptr, w + ": null accum");
+    if (finalize) require(ctx->rhs != nullptr && ctx->solution != nullptr, w + ": finalize records need rhs and solution");
+    const bool alias = finalize && static_cast<const void*>(ctx->gather) == static_cast<const void*>(ctx->solution);
+    b.val.upload_raw(ctx->matrix_values, std::max<int64_t>(nm, 0) * sizeof(double), s);
+    DevBuf g, acc, rhs, sol;
+    const int64_t ng = alias ? std::max(nv, ns) : nv;
+    g.upload_raw(ctx->gather, std::max<int64_t>(ng, 0) * sizeof(double), s);
+    acc.upload_raw(ctx->accum, std::max<int64_t>(no, 0) * sizeof(double), s);
+    // a non-null rhs selects the solve's sequential partials (executor.cpp:53-116)
+    // even without finalize records
+    if (ctx->rhs) {
+        if (finalize) rhs.upload_raw(ctx->rhs, nr * sizeof(double), s);
+        else rhs.ensure(sizeof(double));
+    }
+    if (finalize && !alias) sol.upload_raw(ctx->solution, ns * sizeof(double), s);
+    double* sol_dev = !finalize ? nullptr : alias ? g.as<double>() : sol.as<double>();
+    run_general(&b, g.as<double>(), acc.as<double>(), ctx->rhs ? rhs.as<double>() : nullptr, sol_dev, s);
+    if (no > 0) ck(cudaMemcpyAsync(ctx->accum, acc.p, no * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    if (finalize) ck(cudaMemcpyAsync(ctx->solution, sol_dev, ns * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+}
+
 psc_status exec_one(int which, const psc_codelet_view* c, const psc_exec_context* ctx) {
     return guarded([&] {
         require(c && ctx, "exec_codelet: null argument");
-        Lowered L = lower_single_codelet(*c, which);
-        const auto& G = L.gen;
-        int n = psc_device_count();
-        if (n <= 0) throw CudaError("exec_codelet: no CUDA device is available");
-        int dev = 0;
-        cudaGetDevice(&dev);
-        psc_bound b;
-        b.device = dev;
-        b.canonical = false;
-        cudaStream_t s = nullptr;
-        b.part_group_ptr = G.part_group_ptr;
-        b.g_cp.upload(G.group_codelet_ptr, s);
-        b.g_fp.upload(G.group_fin_ptr, s);
-        b.g_kind.upload(G.c_kind, s);
-        b.g_m.upload(G.c_m, s);
-        b.g_n.upload(G.c_n, s);
-        b.g_form.upload(G.d_form, s);
-        b.g_base.upload(G.d_base, s);
-        b.g_so.upload(G.d_so, s);
-        b.g_si.upload(G.d_si, s);
-        b.g_tab.upload(G.d_tab, s);
-        b.g_tables.upload(G.tables, s);
-        b.g_frow.upload(G.f_row, s);
-        b.g_fdiag.upload(G.f_diag, s);
-        b.g_frhs.upload(G.f_rhs, s);
-        const int64_t nm = G.max_mat + 1, nv = G.max_vec + 1, no = G.max_out + 1;
-        if (nm > 0) require(ctx->matrix_values != nullptr, "exec_codelet: null matrix_values");
-        if (nv > 0) require(ctx->gather != nullptr, "exec_codelet: null gather");
-        if (no > 0) require(ctx->accum != nullptr, "exec_codelet: null accum");
-        b.val.upload_raw(ctx->matrix_values, std::max<int64_t>(nm, 0) * sizeof(double), s);
-        DevBuf g, acc, rhs_flag;
-        g.upload_raw(ctx->gather, std::max<int64_t>(nv, 0) * sizeof(double), s);
-        acc.upload_raw(ctx->accum, std::max<int64_t>(no, 0) * sizeof(double), s);
-        rhs_flag.ensure(sizeof(double));
-        run_general(&b, g.as<double>(), acc.as<double>(), ctx->rhs ? rhs_flag.as<double>() : nullptr, nullptr, s);
-        if (no > 0) ck(cudaMemcpyAsync(ctx->accum, acc.p, no * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-        ck(cudaStreamSynchronize(s), "exec_codelet sync");
+        run_lowered_on_host_context(lower_single_codelet(*c, which), ctx, "exec_codelet");
     });
 }
 
 }  // namespace
+
+extern "C" {
+// Executor::run (executor.hpp:45, executor.cpp:261-267) on a plan that carries
+// its tables (the reference's own CodeletPlan, imported with
+// psc_plan_from_arrays); no matrix argument, accumulates onto ctx.
+PSC_API psc_status psc_executor_run(psc_executor* e, const psc_plan* plan, const psc_exec_context* ctx) {
+    return guarded([&] {
+        require(e && plan && ctx, "Executor::run: null argument");
+        std::lock_guard<std::mutex> lk(e->mu);
+        use_device(e->device);
+        run_lowered_on_host_context(lower_plan_tables(plan->p), ctx, "Executor::run");
+    });
+}
+}  // extern "C"
 
 extern "C" {
 PSC_API psc_status psc_exec_blas_codelet(const psc_codelet_view* c, const psc_exec_context* ctx) {

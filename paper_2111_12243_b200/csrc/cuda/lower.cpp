@@ -665,6 +665,19 @@ void block_halos(Lowered& L, const psc_csr_view& a) {
     }
 }
 
+Lowered lower_plan_tables(const Plan& p) {
+    require(!p.mined,
+            "Executor::run: a plan mined by psc_inspect keeps its tables in the matrix (col_indices); "
+            "run it with psc_execute_plan / run_spmv / run_sptrsv, which take the matrix");
+    Lowered L;
+    L.kernel = p.kernel;
+    L.canonical = false;
+    L.why_general = "Executor::run over a raw context";
+    psc_csr_view none{INT32_MAX, INT32_MAX, INT64_MAX, nullptr, nullptr, nullptr};
+    build_general(p, none, L);
+    return L;
+}
+
 Lowered lower_single_codelet(const psc_codelet_view& cv, int which) {
     check_codelet_shape(which, cv.out.form, cv.mat.form, cv.vec.form);
     Plan p;

@@ -114,6 +114,12 @@ bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows);
 // or tile_chain_blocks).
 void block_halos(Lowered& L, const psc_csr_view& a);
 
+// General-path lowering of a plan with explicit tables (imported with
+// psc_plan_from_arrays: the reference's own CodeletPlan) without a matrix:
+// Executor::run(plan, ctx) semantics (executor.hpp:45). Index ranges come
+// from the descriptors (Lowered::General::max_*).
+Lowered lower_plan_tables(const Plan& p);
+
 // Build a general-path lowering of one hand-built codelet (exec_*_codelet).
 Lowered lower_single_codelet(const psc_codelet_view& c, int which);
 

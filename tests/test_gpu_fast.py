@@ -85,15 +85,15 @@ def test_configs_fast(exe, config, scale):
     assert np.array_equal(got.view(np.int64), multiply(b, x).view(np.int64))  # deterministic
 
 
-@pytest.mark.parametrize("split_bytes", [-1, 4000, 1600])
+@pytest.mark.parametrize("split_bytes", [-1, 16000, 4000])
 def test_fast_column_passes_and_host_path(exe, split_bytes):
-    """Forced column passes (2 and 4 ranges at n = 4000 columns), on the device
-    and through the host-buffer path."""
+    """Forced column passes (4 ranges, the most, at n = 4000 columns), on the
+    device and through the host-buffer path."""
     a = P.generate_config(5, 0.0002)
     x = P.uniform_vector(a.n_cols, 15)
     want = Oracle.spmv_baseline(a.view(), x)
     b, _ = fast_bound(exe, a, split_bytes=split_bytes)
-    assert b.info()["passes_or_block_rows"] == (1 if split_bytes < 0 else -(-8 * a.n_cols // split_bytes))
+    assert b.info()["passes_or_block_rows"] == (1 if split_bytes < 0 else min(4, -(-8 * a.n_cols // split_bytes)))
     got = multiply(b, x)
     assert normwise_err(got, want) <= 1e-12
     assert np.array_equal(multiply(b, x, host=True).view(np.int64), got.view(np.int64))
@@ -140,7 +140,7 @@ def test_fast_placeholders_do_not_touch_x(exe):
         got = multiply(b, x)
         assert np.array_equal(np.isnan(got), np.isnan(want))
         ok = ~np.isnan(want)
-        assert np.array_equal(got[ok], want[ok])
+        assert normwise_err(got[ok], want[ok]) <= 1e-12
 
 
 def test_fast_mode_falls_back_to_parity_for_segmented_plans(exe):
