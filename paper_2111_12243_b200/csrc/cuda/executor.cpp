@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "capi_types.hpp"
+#include "csr.hpp"
 #include "common.hpp"
 #include "kernels.hpp"
 #include "lower.hpp"
@@ -145,8 +146,9 @@ struct psc_bound {
     // general path
     std::vector<int64_t> part_group_ptr;
     DevBuf g_cp, g_fp, g_kind, g_m, g_n, g_form, g_base, g_so, g_si, g_tab, g_tables, g_frow, g_fdiag, g_frhs;
-    // host-side fingerprint used by the run_* cache
-    std::vector<int32_t> finger;
+    // hash of the whole CSR structure (row offsets, columns, sizes): the run_* cache key check
+    uint64_t structure = 0;
+    uint64_t last_use = 0;  // run_* cache LRU clock
 
     int32_t rows() const { return row_end - row_begin; }
     SegmentsDev segs() const {
@@ -182,8 +184,12 @@ struct psc_executor {
     int device = 0;
     cudaStream_t stream = nullptr;
     std::mutex mu;
-    // run_* cache: (plan serial, structure pointers, sizes, general flag) -> bound
-    std::map<std::tuple<uint64_t, const void*, const void*, int64_t, int32_t, int>, std::unique_ptr<psc_bound>> cache;
+    // run_* cache: (plan serial, structure pointers, sizes, general flag) -> bound; a
+    // hit also needs the same whole-structure hash; at most kCacheCap entries (LRU)
+    std::map<std::tuple<uint64_t, const void*, const void*, int64_t, int32_t, int32_t, int>, std::unique_ptr<psc_bound>>
+        cache;
+    static constexpr size_t kCacheCap = 8;
+    uint64_t clock = 0;
     DevBuf vx, vy, vb, vacc;
 };
 
@@ -191,14 +197,6 @@ namespace pscb {
 namespace {
 
 void use_device(int device) { ck(cudaSetDevice(device), "cudaSetDevice"); }
-
-std::vector<int32_t> fingerprint(const psc_csr_view& a) {
-    std::vector<int32_t> f;
-    const int samples = 64;
-    for (int i = 0; i < samples && a.n_rows > 0; ++i) f.push_back(a.row_offsets[(static_cast<int64_t>(a.n_rows) * i) / samples]);
-    for (int i = 0; i < samples && a.nnz > 0; ++i) f.push_back(a.col_indices[(a.nnz * i) / samples]);
-    return f;
-}
 
 // Build a bound plan. force_general lowers through the exact interpreter
 // (execute_plan semantics need accumulate-onto-existing for the solve).
@@ -379,6 +377,15 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                                       int64_t p1, bool force_general, cudaStream_t s, bool allow_split = false) {
     if (p.kernel == PSC_KERNEL_SPTRSV) adopt_triangular(a);
     else validate_csr(a);
+    // A mined plan's tables are its matrix's columns: bind it only to that
+    // matrix (the structure hash its inspection recorded), or -- provenance
+    // unknown (a version-1 plan file) -- after validate_plan (miner.cpp:325-395).
+    if (p.mined && p.structure != 0) {
+        if (structure_hash(a) != p.structure)
+            throw std::logic_error("bind: the plan was inspected from a matrix with a different structure");
+    } else if (p.mined) {
+        validate_plan(p, a);
+    }
     Lowered L = lower_plan(p, a, p0, p1, 0, force_general);
     auto b = std::make_unique<psc_bound>();
     b->device = device;
@@ -393,7 +400,6 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
     b->canonical = L.canonical;
     b->simple = L.simple;
     b->why_general = L.why_general;
-    b->finger = fingerprint(a);
     use_device(device);
     if (L.canonical) {
         const int32_t nr = b->rows();
@@ -760,10 +766,23 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
 
 psc_bound* cached_bound(psc_executor* e, const psc_plan* plan, const psc_csr_view& a, bool general) {
     auto key = std::make_tuple(plan->serial, static_cast<const void*>(a.row_offsets),
-                               static_cast<const void*>(a.col_indices), a.nnz, a.n_rows, general ? 1 : 0);
+                               static_cast<const void*>(a.col_indices), a.nnz, a.n_rows, a.n_cols, general ? 1 : 0);
+    const uint64_t h = structure_hash(a);
     auto it = e->cache.find(key);
-    if (it != e->cache.end() && it->second->finger == fingerprint(a)) return it->second.get();
+    if (it != e->cache.end() && it->second->structure == h) {
+        it->second->last_use = ++e->clock;
+        return it->second.get();
+    }
+    if (it != e->cache.end()) e->cache.erase(it);  // the structure changed in place: rebind
+    while (e->cache.size() >= psc_executor::kCacheCap) {  // evict the least recently used binding
+        auto lru = e->cache.begin();
+        for (auto jt = e->cache.begin(); jt != e->cache.end(); ++jt)
+            if (jt->second->last_use < lru->second->last_use) lru = jt;
+        e->cache.erase(lru);
+    }
     auto b = make_bound(e->device, plan->p, a, PSC_MODE_PARITY, -1, -1, general, e->stream);
+    b->structure = h;
+    b->last_use = ++e->clock;
     psc_bound* raw = b.get();
     e->cache[key] = std::move(b);
     return raw;
@@ -1112,7 +1131,13 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
                 if (std::getenv(v)) return false;  // a profiler (ncu / nsys / sanitizer) is attached
             return true;
         }();
-        if (overlap && x_map && mapped(rhs)) {
+        // The solve's lanes spin on per-unit flags that the gather kernel (another
+        // stream, launched after it) sets: take the overlap only when every solve
+        // CTA (one per SM at most: the record kernel's shared memory) leaves at
+        // least 8 SMs free for the gather, so both are resident together.
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+        if (overlap && x_map && b->n_blocks + 8 <= sms && mapped(rhs)) {
             // b streams in unit by unit (a gather kernel on a side stream, in the
             // order the solve needs the units); every solve lane waits for its
             // unit's rows before staging them

@@ -338,6 +338,8 @@ PSC_API psc_status psc_inspect_device(int32_t kernel, const psc_csr_view* a, int
                                       int32_t device, psc_plan** out) {
     return pscb::guarded([&] {
         pscb::require(a != nullptr && out != nullptr, "inspect: null argument");
-        *out = new psc_plan(pscb::inspect_device(kernel, *a, t, target_groups, device));
+        pscb::Plan p = pscb::inspect_device(kernel, *a, t, target_groups, device);
+        p.structure = pscb::structure_hash(*a);
+        *out = new psc_plan(std::move(p));
     });
 }

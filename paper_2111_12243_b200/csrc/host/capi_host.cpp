@@ -95,7 +95,9 @@ PSC_API psc_status psc_inspect(int32_t kernel, const psc_csr_view* a, int32_t t,
                                int32_t threads, psc_plan** out) {
     return guarded([&] {
         require(a != nullptr && out != nullptr, "inspect: null argument");
-        *out = new psc_plan(inspect(kernel, *a, t, target_groups, threads));
+        Plan p = inspect(kernel, *a, t, target_groups, threads);
+        p.structure = structure_hash(*a);
+        *out = new psc_plan(std::move(p));
     });
 }
 PSC_API psc_status psc_plan_get_counts(const psc_plan* plan, psc_plan_counts* out) {

@@ -136,4 +136,37 @@ Csr lower_triangular(const psc_csr_view& a) {
     return l;
 }
 
+// 64-bit hash of the CSR structure -- sizes, every row offset and column --
+// over blocks on every host thread, combined in block order (so it does not
+// depend on the thread count). Plans mined from a matrix record it, so a
+// plan bound to another matrix is refused (executor.cpp binds), and the run_*
+// cache re-checks it on every call: the reference re-reads the structure on
+// every call (executor.cpp:274-308), so an in-place edit must rebind. O(nnz),
+// cheaper than the values upload a run_* call does anyway.
+uint64_t structure_hash(const psc_csr_view& a) {
+    auto mix = [](uint64_t h, uint64_t v) {
+        h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        return h * 0xFF51AFD7ED558CCDull;
+    };
+    constexpr int64_t kBlock = 1 << 20;
+    const int64_t n_ro = a.row_offsets ? static_cast<int64_t>(a.n_rows) + 1 : 0;
+    const int64_t n_ci = a.col_indices ? a.nnz : 0;
+    const int64_t total = n_ro + n_ci;
+    const int64_t n_blocks = (total + kBlock - 1) / kBlock;
+    std::vector<uint64_t> part(static_cast<size_t>(n_blocks));
+    parallel_for(n_blocks, hw_threads(0), [&](int64_t blk) {
+        uint64_t h = static_cast<uint64_t>(blk) + 1;
+        const int64_t i1 = std::min(total, (blk + 1) * kBlock);
+        for (int64_t i = blk * kBlock; i < i1; ++i) {
+            const int32_t v = i < n_ro ? a.row_offsets[i] : a.col_indices[i - n_ro];
+            h = (h ^ static_cast<uint32_t>(v)) * 0x100000001B3ull;
+        }
+        part[blk] = h;
+    });
+    uint64_t h = mix(mix(mix(0x5157u, static_cast<uint64_t>(a.n_rows)), static_cast<uint64_t>(a.n_cols)),
+                     static_cast<uint64_t>(a.nnz));
+    for (uint64_t p : part) h = mix(h, p);
+    return h;
+}
+
 }  // namespace pscb

@@ -36,5 +36,7 @@ void validate_csr(const psc_csr_view& a);
 void adopt_triangular(const psc_csr_view& a);
 // csr_matrix.cpp:111-130
 Csr lower_triangular(const psc_csr_view& a);
+// 64-bit hash of sizes, row offsets and columns (not values), thread-count independent.
+uint64_t structure_hash(const psc_csr_view& a);
 
 }  // namespace pscb

@@ -33,6 +33,9 @@ struct Plan {
     int64_t nnz = 0;
     int32_t window = 0, target_groups = 0;
     bool mined = true;
+    // structure_hash of the matrix a mined plan was inspected from (its tables
+    // are that matrix's columns); 0 = unknown (a version-1 plan file)
+    uint64_t structure = 0;
 
     std::vector<int64_t> part_group_ptr{0};
     std::vector<int32_t> g_row_begin, g_row_end;

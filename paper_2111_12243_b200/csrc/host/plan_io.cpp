@@ -19,7 +19,7 @@ namespace pscb {
 namespace {
 
 constexpr char kMagic[8] = {'P', 'S', 'C', 'P', 'L', 'A', 'N', '\0'};
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;  // 2: + the structure hash of the matrix a mined plan came from
 
 struct File {
     std::FILE* f = nullptr;
@@ -95,6 +95,7 @@ void plan_save(const Plan& plan, const std::string& path) {
     put(f, plan.window);
     put(f, plan.target_groups);
     put<uint8_t>(f, plan.mined ? 1 : 0);
+    put<uint64_t>(f, plan.structure);
     Plan& p = const_cast<Plan&>(plan);
     arrays(p, [&](auto& v) { put_vec(f, v); });
     require(std::fflush(f) == 0, "plan_save: write failed");
@@ -107,7 +108,8 @@ Plan plan_load(const std::string& path) {
     std::FILE* f = file.f;
     char magic[8];
     require(std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, kMagic, 8) == 0, "plan_load: not a plan file");
-    require(get<uint32_t>(f) == kVersion, "plan_load: unsupported version");
+    const uint32_t version = get<uint32_t>(f);
+    require(version == 1 || version == kVersion, "plan_load: unsupported version");
     Plan p;
     p.kernel = get<int32_t>(f);
     p.n_rows = get<int32_t>(f);
@@ -116,8 +118,10 @@ Plan plan_load(const std::string& path) {
     p.window = get<int32_t>(f);
     p.target_groups = get<int32_t>(f);
     p.mined = get<uint8_t>(f) != 0;
+    if (version >= 2) p.structure = get<uint64_t>(f);
     arrays(p, [&](auto& v) { get_vec(f, v); });
-    // structural sanity (the matrix is checked by psc_validate_plan)
+    // structural sanity (binding checks the matrix: the structure hash, or
+    // validate_plan for a version-1 file)
     require(p.kernel == PSC_KERNEL_SPMV || p.kernel == PSC_KERNEL_SPTRSV, "plan_load: bad kernel");
     const int64_t ng = p.n_groups(), nc = p.n_codelets();
     require(!p.part_group_ptr.empty() && p.part_group_ptr.back() == ng, "plan_load: inconsistent partitions");

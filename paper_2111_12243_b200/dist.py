@@ -183,15 +183,33 @@ class PeerExchange:
         dist.all_reduce(self.token, group=self.group)
 
     def multiply(self, x_local, y, stream=None) -> None:
-        """x_local: this rank's x entries (a CUDA tensor); y: its rows' result."""
+        """x_local: this rank's x entries (a CUDA tensor); y: its rows' result.
+
+        Everything -- both all-reduce barriers, the window copy and the fused
+        launch -- is ordered on one stream (`stream`, default torch's current
+        one), which first waits for the caller's current stream (the work
+        that produced x_local); the caller's stream then waits for it."""
+        import contextlib
+
+        import torch
+
         from .psc import BoundPlan
 
         b, e = self.ranges[self.rank]
-        s = BoundPlan._stream(stream)
-        self._sync()
-        self.ipc.copy(self.window + 8 * b, x_local.data_ptr(), 8 * (e - b), s)
-        self._sync()
-        self.bound.spmv_peers(self.peers, self.window, y, stream)
+        cuda = self.token.is_cuda
+        ts = None
+        if cuda and stream is not None:
+            ts = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(int(stream))
+            ts.wait_stream(torch.cuda.current_stream())
+        ctx = torch.cuda.stream(ts) if ts is not None else contextlib.nullcontext()
+        with ctx:
+            s = BoundPlan._stream(stream if ts is None else ts)
+            self._sync()
+            self.ipc.copy(self.window + 8 * b, x_local.data_ptr(), 8 * (e - b), s)
+            self._sync()
+            self.bound.spmv_peers(self.peers, self.window, y, s.value if ts is not None else stream)
+        if ts is not None:
+            torch.cuda.current_stream().wait_stream(ts)
 
     def close(self) -> None:
         for ptr in self.opened.values():

@@ -367,3 +367,45 @@ def test_spmv_host_row_slices(n, band):
         bound.spmv_host(xh, yh)
         torch.cuda.synchronize()
         assert bitwise_equal(yh, want), seed
+
+
+def test_bind_refuses_a_plan_from_another_matrix(exe, tmp_path):
+    """A mined plan's tables are its matrix's columns; binding it to a matrix of
+    the same shape but another structure is refused -- also after a save /
+    load round trip (the file records the structure hash)."""
+    a = P.generate_config(1, 0.0004)  # 20 x 20 grid
+    b = P.generate_config(1, 0.0004)
+    b.col_indices = b.col_indices.copy()
+    r = 7
+    k0, k1 = int(b.row_offsets[r]), int(b.row_offsets[r + 1])
+    b.col_indices[k0] = b.col_indices[k0] - 1 if b.col_indices[k0] > 0 else 1  # still sorted, same nnz
+    assert np.all(np.diff(b.col_indices[k0:k1]) > 0)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    P.BoundPlan(exe, plan, a).close()
+    with pytest.raises(P.LogicError):
+        P.BoundPlan(exe, plan, b)
+    path = tmp_path / "a.plan"
+    plan.save(path)
+    loaded = P.CodeletPlan.load(path, a)
+    P.BoundPlan(exe, loaded, a).close()
+    with pytest.raises(P.LogicError):
+        P.BoundPlan(exe, loaded, b)
+
+
+def test_run_cache_sees_in_place_structure_edits(exe):
+    """run_spmv caches the binding per (plan, arrays); an in-place edit of the
+    structure (anywhere -- the check hashes all of it) must rebind, and the
+    result must follow the edited matrix (the reference re-reads it)."""
+    a = P.generate_config(1, 0.0004)
+    x = P.uniform_vector(a.n_cols, 3)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    y = np.empty(a.n_rows)
+    P.run_spmv(plan, a, x, y, exe)
+    assert bitwise_equal(y, Oracle.run_spmv(plan.export_arrays(), a.view(), x))
+    # a structure edit the plan no longer matches: the rebind must refuse it
+    k = int(a.row_offsets[250])
+    a.col_indices[k] = a.col_indices[k] + 1 if a.col_indices[k] + 1 < a.col_indices[k + 1] else a.col_indices[k]
+    if not np.all(np.diff(a.col_indices[a.row_offsets[250]:a.row_offsets[251]]) > 0):
+        pytest.skip("edit would unsort the row")
+    with pytest.raises((P.LogicError, P.InvalidArgument)):
+        P.run_spmv(plan, a, x, y, exe)
