@@ -114,7 +114,8 @@ struct psc_bound {
     DevBuf q_units, q_ends, q_next;  // trsv_lean == 4: global unit queue (chain starts / ends)
     int n_q_units = 0;
     int q_backoff = 200;  // ns a queue warp sleeps between polls of a missing operand (PSC_TRSV_BACKOFF)
-    DevBuf s_pieces;      // trsv_lean == 4, chain mode: <= 32-row pieces of the chain units (streaming kernel)
+    DevBuf s_pieces, s_w0;  // trsv_lean == 4, chain mode: <= 32-row pieces of the chain units (streaming kernel),
+                            // and each piece's window start (its chain's previous piece)
     int n_s_pieces = 0;   // 0: the warp-per-row queue kernel
     int stream_k = 8;     // entries a lane consumes per round
     DevBuf unit_len, unit_loc, row_block, row_loc;  // trsv_lean == 2: unit tables, row -> (block, window slot)
@@ -168,7 +169,7 @@ struct psc_bound {
     }
     int64_t device_bytes() const {
         size_t t = 0;
-        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &sp_ro[0], &sp_ro[1], &sp_ro[2], &sp_ro[3], &sp_col[0], &sp_col[1], &sp_col[2], &sp_col[3], &sp_val[0], &sp_val[1], &sp_val[2], &sp_val[3], &sp_j0[1], &sp_j0[2], &sp_j0[3], &sp_state, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
+        for (const DevBuf* b : {&ro, &col, &val, &rsp, &sst, &slen, &svec, &chunk_row, &item_seg, &long_list, &groups, &sp_ro[0], &sp_ro[1], &sp_ro[2], &sp_ro[3], &sp_col[0], &sp_col[1], &sp_col[2], &sp_col[3], &sp_val[0], &sp_val[1], &sp_val[2], &sp_val[3], &sp_j0[1], &sp_j0[2], &sp_j0[3], &sp_state, &ticket, &armed, &block_row, &block_unit, &unit_start, &rec, &q_units, &q_ends, &s_pieces, &s_w0, &g_order, &unit_len, &unit_loc, &row_block, &row_loc, &remote_block, &remote_item, &remote_long, &halo_ptr, &halo_col, &halo_key, &halo_pos, &g_cp, &g_fp,
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
@@ -547,11 +548,15 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                     // streaming kernel (lane per row): the chains cut into pieces of <= 32 rows
                     const char* sv = std::getenv("PSC_TRSV_STREAM");
                     if (!(sv && sv[0] == '0')) {
-                        std::vector<int32_t> pieces;
+                        std::vector<int32_t> pieces, w0;
                         for (size_t i = 0; i < units.size(); ++i)
-                            for (int32_t r = units[i]; r < en[i]; r += 32) pieces.push_back(r);
+                            for (int32_t r = units[i]; r < en[i]; r += 32) {
+                                pieces.push_back(r);
+                                w0.push_back(r == units[i] ? r : r - 32);  // the previous piece of the chain
+                            }
                         pieces.push_back(nr);
                         b->s_pieces.upload(pieces, s);
+                        b->s_w0.upload(w0, s);
                         b->n_s_pieces = static_cast<int>(pieces.size()) - 1;
                     }
                 } else {
@@ -655,7 +660,7 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             b->ticket.ensure(2 * sizeof(int32_t));
             ck(cudaMemsetAsync(b->ticket.p, 0, 2 * sizeof(int32_t), s), "memset");
             if (const char* tr = std::getenv("PSC_TRSV_TRACE"); tr && tr[0] == '1') {
-                const size_t nt = static_cast<size_t>(b->rows()) + b->n_blocks + 8;
+                const size_t nt = static_cast<size_t>(b->rows()) + b->n_blocks + 16;
                 b->trace.ensure(nt * sizeof(unsigned long long));
                 ck(cudaMemsetAsync(b->trace.p, 0, nt * sizeof(unsigned long long), s), "memset");
             }
@@ -734,7 +739,7 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
     use_device(b->device);
     if (b->canonical && b->trsv_lean == 4 && b->n_s_pieces > 0) {
         launch_sptrsv_stream(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,
-                             b->s_pieces.as<int32_t>(), b->n_s_pieces, b->segs(), b->q_next.as<int>(),
+                             b->s_pieces.as<int32_t>(), b->s_w0.as<int32_t>(), b->n_s_pieces, b->segs(), b->q_next.as<int>(),
                              b->trace.as<unsigned long long>(), b->rows(), b->n_sms, b->stream_k, s);
     } else if (b->canonical && b->trsv_lean == 4) {
         launch_sptrsv_queue(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, acc,

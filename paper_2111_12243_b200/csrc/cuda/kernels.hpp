@@ -110,8 +110,11 @@ void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, con
 // (units[n_units] = n_rows) or single rows, in topological order.
 // Lane-per-row streaming solve over pieces of <= 32 consecutive rows
 // (boundaries in `pieces`, n_pieces + 1 entries, in row order).
+// piece_w0 (nullable): per piece, the first row of the previous piece of the
+// same chain (== the piece's first row when it starts a chain)
 void launch_sptrsv_stream(const int32_t* ro, const int32_t* col, const double* val, const double* b, double* x,
-                          double* acc_out, const int32_t* pieces, int n_pieces, SegmentsDev s, int* next_unit,
+                          double* acc_out, const int32_t* pieces, const int32_t* piece_w0, int n_pieces, SegmentsDev s,
+                          int* next_unit,
                           unsigned long long* trace, int n_rows, int n_sms, int k_entries, cudaStream_t stream);
 void launch_sptrsv_queue(const int32_t* ro, const int32_t* col, const double* val, const double* b, double* x,
                          double* acc_out, const int32_t* units, const int32_t* unit_end, int n_units,

@@ -25,7 +25,7 @@ for _ in range(2):
     bound.sptrsv(b, x)
 torch.cuda.synchronize()
 n, nb = a.n_rows, bound.info()["work_units"]
-buf = np.zeros(n + nb + 8, dtype=np.uint64)
+buf = np.zeros(n + nb + 16, dtype=np.uint64)
 _capi.lib().psc_bound_trace(bound._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size)
 t = buf[:n].astype(np.int64)
 t -= t.min()
@@ -87,7 +87,9 @@ while last_dep[r] >= 0:
     r = d
 print(f"critical path: {hops_same} in-piece hops ({t_same / 1e6:.2f} ms, {t_same / max(hops_same, 1):.0f} ns each), "
       f"{hops_other} cross-piece hops ({t_other / 1e6:.2f} ms, {t_other / max(hops_other, 1):.0f} ns each)")
-st4 = buf[n:n + 4].astype(np.float64)  # streaming kernel: rounds with / without L2 operand loads, and their cycles
+st4 = buf[n:n + 9].astype(np.float64)
+print(f"triangle phases: {st4[7] / max(st4[4], 1):.0f} cycles each, {st4[7] / max(st4[8], 1):.0f} cycles per column")
+print(f"pieces (2 solves): {st4[6]:.0f}; finished by the triangle phase {st4[4]:.0f}, of them with the previous piece in the window {st4[5]:.0f}")  # streaming kernel: rounds with / without L2 operand loads, and their cycles
 if st4[0] + st4[2] > 0:
     print(f"stream rounds (2 solves, all warps): with L2 loads {st4[0]:.0f} ({st4[1] / max(st4[0], 1):.0f} cycles each), "
           f"smem only {st4[2]:.0f} ({st4[3] / max(st4[2], 1):.0f} cycles each)")
