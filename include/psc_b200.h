@@ -306,6 +306,9 @@ PSC_API psc_status psc_exec_pscii_codelet(const psc_codelet_view* c, const psc_e
  * sptrsv_csr_baseline (executor.cpp:310-340); device pointers. */
 PSC_API psc_status psc_csr_spmv_device(const psc_bound* b, const double* x_dev, double* y_dev,
                                        void* stream);
+/* Forward substitution, one thread per row, sync-free (b: an SpTRSV bound
+ * plan; its CSR is used, the plan is not). x_dev is overwritten. */
+PSC_API psc_status psc_csr_sptrsv_device(psc_bound* b, const double* b_dev, double* x_dev, void* stream);
 
 /* ---- matrices: construction, validation, Matrix Market, benchmark configs -- */
 typedef struct psc_csr psc_csr; /* owned CSR */

@@ -161,6 +161,7 @@ _SIGS = {
     "psc_exec_psci_codelet": (c_int32, [POINTER(CodeletView), POINTER(ExecContext)]),
     "psc_exec_pscii_codelet": (c_int32, [POINTER(CodeletView), POINTER(ExecContext)]),
     "psc_csr_spmv_device": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "psc_csr_sptrsv_device": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "psc_csr_view_of": (c_int32, [c_void_p, POINTER(CsrView)]),
     "psc_csr_destroy": (None, [c_void_p]),
     "psc_csr_from_triplets": (

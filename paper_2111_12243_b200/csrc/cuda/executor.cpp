@@ -108,8 +108,7 @@ struct psc_bound {
     int32_t epoch = 0;      // per-launch arming epoch of the solve kernel
     DevBuf trace;           // PSC_TRSV_TRACE=1: per-row publish times (diagnostics)
     int trsv_threads = 256; // CTA size of the solve kernel (PSC_TRSV_THREADS)
-    int trsv_lat = 700;     // cycles before a lane inspects a load it issued (PSC_TRSV_LAT)
-    int trsv_lean = 0;      // round kernel for simple rows with <= 4 off-diagonal entries: 1 probed, 2 records
+    int trsv_lean = 0;      // solve kernel: 2 records (sptrsv_rec_kernel), 4 global queue (streaming / unit queue)
     DevBuf rec;             // trsv_lean == 2: per-row records (trsv_pack_kernel)
     DevBuf q_units, q_ends, q_next;  // trsv_lean == 4: global unit queue (chain starts / ends)
     int n_q_units = 0;
@@ -124,6 +123,7 @@ struct psc_bound {
     bool tiled = false;     // blocks grown over the unit graph (not row ranges)
     bool rec_dirty = true;  // values changed since the records were packed
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
+    DevBuf naive_ticket;    // psc_csr_sptrsv_device
     // overlapped upload of b (host path, record kernel): copy stream, chunk flags
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_before = nullptr, ev_copied = nullptr;
@@ -503,23 +503,55 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
             }
             cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
         } else {
-            // Solve-round kernel: records (lean 2) for simple rows with <= 4
-            // off-diagonal entries whose block window (rows + halo) fits in
-            // shared memory; probed rounds (lean 1) for other simple short
-            // rows; generic rounds otherwise. Record kernels in chain mode take
-            // tiled blocks (tile_chain_blocks).
+            // Solve kernel: the record kernel (sptrsv_rec_kernel) for simple rows
+            // with <= 4 off-diagonal entries whose block window (rows + halo) fits
+            // in shared memory -- in chain mode over tiled blocks
+            // (tile_chain_blocks); every other canonical plan goes to a global
+            // queue: the streaming kernel (chain mode, lane per row) or the unit
+            // queue (row mode). PSC_TRSV_LEAN=4 forces the queue.
             int32_t max_ext = 0;
             for (int32_t r = L.row_begin; r < L.row_end; ++r)
                 max_ext = std::max(max_ext, a.row_offsets[r + 1] - a.row_offsets[r] - 1);
-            const bool lean = L.simple && max_ext <= 4;
-            // rows the record kernel cannot take: a global queue of units, one
-            // warp each (kernel 4); kernel 3 = warp per unit inside row blocks
-            int want = lean ? 2 : 4;
-            if (const char* ln = std::getenv("PSC_TRSV_LEAN")) {
-                const int v = std::max(0, std::atoi(ln));
-                want = lean ? std::min(2, v) : (v >= 3 ? std::min(v, 4) : 0);
+            bool want_rec = L.simple && max_ext <= 4;
+            if (const char* ln = std::getenv("PSC_TRSV_LEAN")) want_rec = want_rec && std::atoi(ln) != 4;
+            auto pick_threads = [&](const Lowered& M, int max_halo) {
+                int th = 256;
+                if (M.chain_mode) {  // enough lanes for the units of a block
+                    th = 64;
+                    while (th < 512 && th < M.max_block_units) th *= 2;
+                }
+                if (const char* env = std::getenv("PSC_TRSV_THREADS")) th = std::atoi(env);
+                int p2 = 64;  // the solve kernels are instantiated for 64, 128, 256 and 512 threads
+                while (p2 < 512 && p2 < th) p2 *= 2;
+                th = p2;
+                while (th > 64 && sptrsv_smem_bytes(th, M.max_block_rows, M.max_block_units, max_halo) > 232448) th /= 2;
+                return sptrsv_smem_bytes(th, M.max_block_rows, M.max_block_units, max_halo) <= 232448 ? th : -1;
+            };
+            auto recs_fit = [&](Lowered& M) {  // window indices fit int16 and the window fits
+                block_halos(M, a);
+                return M.max_block_rows + M.max_block_halo <= 32767 && pick_threads(M, M.max_block_halo) > 0;
+            };
+            b->trsv_lean = 4;
+            if (want_rec) {
+                bool tiles = L.chain_mode;
+                if (const char* tv = std::getenv("PSC_TRSV_TILES")) tiles = tiles && tv[0] != '0';
+                if (tiles) {
+                    Lowered T = L;
+                    if (tile_chain_blocks(T, a, L.max_block_rows) && recs_fit(T)) {
+                        L = std::move(T);
+                        b->trsv_lean = 2;
+                    }
+                }
+                if (b->trsv_lean != 2) {
+                    Lowered C = L;
+                    unit_maps(C);
+                    if (recs_fit(C)) {
+                        L = std::move(C);
+                        b->trsv_lean = 2;
+                    }
+                }
             }
-            if (want == 4) {
+            if (b->trsv_lean == 4) {
                 // units over the whole matrix: chains in row order (chain mode) or
                 // single rows by dependency level (row mode); both topological
                 const int32_t nr = L.row_end - L.row_begin;
@@ -571,51 +603,6 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 if (const char* bo = std::getenv("PSC_TRSV_BACKOFF")) b->q_backoff = std::max(0, std::atoi(bo));
                 cudaDeviceGetAttribute(&b->n_sms, cudaDevAttrMultiProcessorCount, device);
             }
-            if (want == 3) {  // blocks of ~32 units (two per warp)
-                const int64_t n_units = static_cast<int64_t>(L.unit_start.size());
-                const double avg = n_units ? static_cast<double>(L.row_end - L.row_begin) / static_cast<double>(n_units) : 1.0;
-                int R3 = static_cast<int>(std::min(8192.0, std::max(256.0, 32.0 * avg)));
-                if (const char* env = std::getenv("PSC_SPTRSV_BLOCK_ROWS")) R3 = std::atoi(env);
-                L = lower_plan(p, a, p0, p1, R3, force_general);
-            }
-            auto pick_threads = [&](const Lowered& M, int max_halo) {
-                int th = 256;
-                if (M.chain_mode) {  // enough lanes for the units of a block
-                    th = 64;
-                    while (th < 512 && th < M.max_block_units) th *= 2;
-                }
-                if (const char* env = std::getenv("PSC_TRSV_THREADS")) th = std::atoi(env);
-                int p2 = 64;  // the solve kernels are instantiated for 64, 128, 256 and 512 threads
-                while (p2 < 512 && p2 < th) p2 *= 2;
-                th = p2;
-                while (th > 64 && sptrsv_smem_bytes(th, M.max_block_rows, M.max_block_units, max_halo) > 232448) th /= 2;
-                return sptrsv_smem_bytes(th, M.max_block_rows, M.max_block_units, max_halo) <= 232448 ? th : -1;
-            };
-            auto recs_fit = [&](Lowered& M) {  // window indices fit int16 and the window fits
-                block_halos(M, a);
-                return M.max_block_rows + M.max_block_halo <= 32767 && pick_threads(M, M.max_block_halo) > 0;
-            };
-            b->trsv_lean = want >= 3 ? want : (lean ? 1 : 0);
-            if (want == 2) {
-                bool tiles = L.chain_mode;
-                if (const char* tv = std::getenv("PSC_TRSV_TILES")) tiles = tiles && tv[0] != '0';
-                if (tiles) {
-                    Lowered T = L;
-                    if (tile_chain_blocks(T, a, L.max_block_rows) && recs_fit(T)) {
-                        L = std::move(T);
-                        b->trsv_lean = 2;
-                    }
-                }
-                if (b->trsv_lean != 2) {
-                    Lowered C = L;
-                    unit_maps(C);
-                    if (recs_fit(C)) {
-                        L = std::move(C);
-                        b->trsv_lean = 2;
-                    }
-                }
-            }
-            if (want < b->trsv_lean && want < 3) b->trsv_lean = want;
             b->n_blocks = static_cast<int>(L.block_row.size()) - 1;
             b->chain_mode = L.chain_mode;
             b->tiled = L.tiled;
@@ -653,9 +640,11 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 b->max_block_halo = L.max_block_halo;
                 b->rec.ensure(static_cast<size_t>(b->rows()) * trsv_rec_bytes());
             }
-            const int th = pick_threads(L, b->max_block_halo);
-            require(th > 0, "bind: solve block does not fit in shared memory");
-            b->trsv_threads = th;
+            if (b->trsv_lean == 2) {
+                const int th = pick_threads(L, b->max_block_halo);
+                require(th > 0, "bind: solve block does not fit in shared memory");
+                b->trsv_threads = th;
+            }
             b->max_block_rows = L.max_block_rows;
             b->ticket.ensure(2 * sizeof(int32_t));
             ck(cudaMemsetAsync(b->ticket.p, 0, 2 * sizeof(int32_t), s), "memset");
@@ -664,7 +653,6 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 b->trace.ensure(nt * sizeof(unsigned long long));
                 ck(cudaMemsetAsync(b->trace.p, 0, nt * sizeof(unsigned long long), s), "memset");
             }
-            if (const char* tl = std::getenv("PSC_TRSV_LAT")) b->trsv_lat = std::atoi(tl);
             b->armed.ensure(std::max(1, b->n_blocks) * sizeof(int32_t));
             ck(cudaMemsetAsync(b->armed.p, 0, std::max(1, b->n_blocks) * sizeof(int32_t), s), "memset");
         }
@@ -758,9 +746,9 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
                       b->block_row.as<int32_t>(), b->block_unit.as<int32_t>(), b->unit_start.as<int32_t>(), b->n_blocks,
                       b->max_block_rows, b->max_block_units, !b->chain_mode, b->segs(), b->ticket.as<int32_t>(),
                       b->armed.as<int32_t>(), b->epoch, b->trace.as<unsigned long long>(), b->trsv_threads,
-                      b->trsv_lat, b->trsv_lean, b->rec.p, b->unit_len.as<int32_t>(),
+                      b->rec.p, b->unit_len.as<int32_t>(),
                       b->unit_loc.as<int32_t>(), b->halo_ptr.as<int32_t>(), b->halo_col.as<int32_t>(), b->max_block_halo,
-                      b->trsv_lean == 2 ? x_host : nullptr, b_ready, b_shift, b_flag, s);
+                      x_host, b_ready, b_shift, b_flag, s);
     } else {
         require(acc != nullptr, "sptrsv: the general path needs an acc buffer");
         ck(cudaMemsetAsync(acc, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset acc");
@@ -1228,6 +1216,19 @@ PSC_API psc_status psc_csr_spmv_device(const psc_bound* b, const double* x, doub
         launch_csr_spmv_naive(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y, b->rows(),
                               static_cast<cudaStream_t>(stream));
         ck(cudaGetLastError(), "csr_spmv launch");
+    });
+}
+
+PSC_API psc_status psc_csr_sptrsv_device(psc_bound* b, const double* rhs, double* x, void* stream) {
+    return guarded([&] {
+        require(b && rhs && x, "csr_sptrsv: null argument");
+        require(b->canonical, "csr_sptrsv: needs a canonical bound plan");
+        require(b->kernel == PSC_KERNEL_SPTRSV, "csr_sptrsv: plan was built for another kernel");
+        use_device(b->device);
+        b->naive_ticket.ensure(sizeof(int));
+        launch_csr_sptrsv_naive(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), rhs, x, b->rows(),
+                                b->naive_ticket.as<int>(), static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "csr_sptrsv launch");
     });
 }
 

@@ -92,20 +92,19 @@ void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val
                         int short_rows, int n_rows, cudaStream_t stream,
                         const PeerDev* peer = nullptr);
 
-// Sync-free blocked triangular solve (kernels.cu, "blocked sync-free
-// triangular solve"): blocks [block_row[i], block_row[i+1]) of rows, solved by
-// units listed in unit_start[block_unit[i] .. block_unit[i+1]) -- runs of
-// consecutive rows (chain mode) or single rows in level order
-// (single_row_units). ticket: 2 zeroed ints, left zeroed; armed: one int per
-// block, epoch a per-launch counter. trace (nullable) gets per-row publish
-// times followed by one arm time per block.
+// Sync-free blocked record solve (kernels.cu sptrsv_rec_kernel): blocks of
+// rows (block_row: prefix sums of block sizes), solved by units listed in
+// unit_start[block_unit[i] .. block_unit[i+1]) -- runs of consecutive rows
+// (chain mode) or single rows in level order (single_row_units) -- from the
+// per-row records (trsv_pack_kernel). ticket: 2 zeroed ints, left zeroed;
+// armed: one int per block, epoch a per-launch counter. trace (nullable) gets
+// per-row publish times followed by one arm time per block.
 void launch_sptrsv(const int32_t* ro, const int32_t* col, const double* val, const double* b, double* x,
                    double* acc_out, const int32_t* block_row, const int32_t* block_unit, const int32_t* unit_start,
                    int n_blocks, int max_rows, int max_units, bool single_row_units, SegmentsDev segs,
-                   int32_t* ticket, int32_t* armed, int epoch, unsigned long long* trace, int threads,
-                   int poll_latency, int lean, const void* rec, const int32_t* unit_len,
-                   const int32_t* unit_loc, const int32_t* halo_ptr, const int32_t* halo_col, int max_halo,
-                   double* x_host, const int* b_ready, int b_shift, int b_flag, cudaStream_t stream);
+                   int32_t* ticket, int32_t* armed, int epoch, unsigned long long* trace, int threads, const void* rec,
+                   const int32_t* unit_len, const int32_t* unit_loc, const int32_t* halo_ptr, const int32_t* halo_col,
+                   int max_halo, double* x_host, const int* b_ready, int b_shift, int b_flag, cudaStream_t stream);
 // Global unit queue solve (long rows): units = first rows of the chains
 // (units[n_units] = n_rows) or single rows, in topological order.
 // Lane-per-row streaming solve over pieces of <= 32 consecutive rows
@@ -133,7 +132,7 @@ void launch_trsv_pack(const int32_t* ro, const int32_t* col, const double* val, 
                       const int32_t* halo_pos, int n_rows, void* rec, cudaStream_t stream);
 // mismatches between the record kernel's division and __ddiv_rn on n random operand pairs (-1: CUDA error)
 int64_t division_selftest(uint64_t seed, int64_t n, int exp_span);
-size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units, int max_halo = -1);  // max_halo >= 0: record kernel
+size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units, int max_halo);  // record kernel
 
 // General interpreter (exact Listing-3 semantics) over groups [g0, g1) of one
 // partition; one thread per region group.
@@ -158,6 +157,9 @@ void launch_general_partition(GeneralDev g, int64_t g0, int64_t g1, const double
                               cudaStream_t stream);
 
 // Naive row-sequential CSR SpMV (spmv_csr_baseline, executor.cpp:310-323).
+// sptrsv_csr_baseline on the GPU: thread per row, sync-free (ticket: 1 int).
+void launch_csr_sptrsv_naive(const int32_t* ro, const int32_t* col, const double* val, const double* b, double* x,
+                             int32_t n_rows, int* ticket, cudaStream_t stream);
 void launch_csr_spmv_naive(const int32_t* ro, const int32_t* col, const double* val, const double* x,
                            double* y, int32_t n_rows, cudaStream_t stream);
 

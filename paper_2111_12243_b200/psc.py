@@ -797,8 +797,14 @@ class BoundPlan:
         _check(_capi.lib().psc_bound_sptrsv_host(self._h, _dp(b), _dp(x), _dp(acc), self._stream(stream)))
 
     def csr_spmv_naive(self, x, y, stream=None) -> None:
+        """spmv_csr_baseline on the GPU (executor.cpp:310-322) over this plan's matrix."""
         _check(_capi.lib().psc_csr_spmv_device(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
                                                self._stream(stream)))
+
+    def csr_sptrsv_naive(self, b, x, stream=None) -> None:
+        """sptrsv_csr_baseline on the GPU (executor.cpp:325-340): thread per row, sync-free."""
+        _check(_capi.lib().psc_csr_sptrsv_device(self._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()),
+                                                 self._stream(stream)))
 
     def launches(self) -> int:
         return int(_capi.lib().psc_bound_launches(self._h))

@@ -119,7 +119,7 @@ def test_sptrsv_mixed_short_and_long_rows(monkeypatch, stream):
     _sptrsv_check(exe, _lower(1000, rows))
 
 
-@pytest.mark.parametrize("lean", ["0", "1", "2", "4"])
+@pytest.mark.parametrize("lean", ["2", "4"])
 def test_sptrsv_kernels_on_chain_and_stencil(monkeypatch, lean):
     monkeypatch.setenv("PSC_TRSV_LEAN", lean)
     exe = P.Executor(1)

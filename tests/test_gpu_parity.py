@@ -301,11 +301,12 @@ def test_division_matches_ieee():
         assert bad.value == 0, (span, bad.value)
 
 
-@pytest.mark.parametrize("lean", ["0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("lean", ["2", "4"])
 @pytest.mark.parametrize("block_rows", ["1024", "0"])
 def test_sptrsv_round_kernels_bitwise(monkeypatch, lean, block_rows):
-    """Every solve-round kernel (generic, probed, record-driven), with default
-    and small blocks (many operands from earlier blocks), equals the oracle."""
+    """Both solve kernels (records where they apply, PSC_TRSV_LEAN=2; the
+    streaming / unit queue, 4), with default and small blocks (many operands
+    from earlier blocks), equal the oracle."""
     monkeypatch.setenv("PSC_TRSV_LEAN", lean)
     if block_rows != "0":
         monkeypatch.setenv("PSC_SPTRSV_BLOCK_ROWS", block_rows)
