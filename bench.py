@@ -386,8 +386,21 @@ def run_ours(args):
     # ---- e2e: the public host-buffer API (H2D input, kernels, D2H result) ----
     e2e_check = None
     if sharded:
-        e2e_ms = step_ms.copy()  # x already device-resident per rank; reported as the exchange+compute step
-        h2d = d2h = 0
+        # per rank: its x slice up from pinned host memory, the exchange and the
+        # shard's multiply, its y rows back down
+        host_in = torch.from_numpy(vec_h[bound.row_begin:bound.row_end].copy()).pin_memory()
+        host_out = torch.empty(max(rows, 1), dtype=torch.float64).pin_memory()
+        dev_in = torch.empty_like(x_mine)
+
+        def e2e_step():
+            dev_in.copy_(host_in, non_blocking=True)
+            bound.spmv(xex.exchange(dev_in), out)
+            host_out.copy_(out, non_blocking=True)
+
+        e2e_ms, _, _ = timed(e2e_step, args.steps, args.warmup, True)
+        h2d, d2h = 8 * rows, 8 * rows
+        e2e_check = "bitwise equal to the device path" if np.array_equal(
+            host_out.numpy()[:rows].view(np.int64), got.view(np.int64)) else "MISMATCH"
     else:
         host_in = torch.from_numpy(vec_h.copy()).pin_memory()
         host_out = torch.empty(max(rows, 1), dtype=torch.float64).pin_memory()

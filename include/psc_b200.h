@@ -177,6 +177,13 @@ PSC_API psc_status psc_plan_load(const char* path, psc_plan** out);
  * it, so results are bitwise identical for every value (executor.hpp:29-35). */
 PSC_API psc_status psc_executor_create(int32_t workers, int32_t device, psc_executor** out);
 PSC_API int32_t psc_executor_workers(const psc_executor* exec);
+/* The run_* / execute_plan calls read the matrix values on every call, as the
+ * reference does (they may change between calls). A caller whose values do
+ * not change tags them with a nonzero version: a call whose bound plan already
+ * holds values of that version skips their upload; any other version uploads
+ * them again. 0 (the default) means "unknown": always upload. Not in the
+ * reference (it has no device copy to keep). */
+PSC_API psc_status psc_executor_set_values_version(psc_executor* exec, uint64_t version);
 PSC_API void psc_executor_destroy(psc_executor* exec);
 
 /* Bind a plan and its matrix: lowers the plan to device segments and uploads
@@ -205,7 +212,9 @@ PSC_API psc_status psc_bound_sptrsv(psc_bound* b, const double* b_dev, double* x
                                     double* acc_dev /* nullable */, void* stream);
 /* Host-buffer variants (the end-to-end path): H2D of the input vector, the
  * kernel, and D2H of the result, enqueued on `stream` (pinned host memory
- * makes the copies asynchronous). */
+ * makes the copies asynchronous). They share the bound's scratch buffers:
+ * calls on one bound from several threads or streams are serialised, each
+ * enqueued after the previous call's work. */
 PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x_host, double* y_host, void* stream);
 PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* b_host, double* x_host,
                                          double* acc_host /* nullable */, void* stream);

@@ -152,6 +152,8 @@ class Executor {
         e_.reset(e);
     }
     int workers() const { return psc_executor_workers(e_.get()); }
+    // psc_executor_set_values_version: skip re-uploading unchanged matrix values
+    void set_values_version(uint64_t version) { check(psc_executor_set_values_version(e_.get(), version)); }
     psc_executor* handle() const { return e_.get(); }
 
     // Executor::run (executor.hpp:45): the plan over a raw ExecutionContext,

@@ -123,6 +123,7 @@ _SIGS = {
     "psc_plan_destroy": (None, [c_void_p]),
     "psc_executor_create": (c_int32, [c_int32, c_int32, POINTER(c_void_p)]),
     "psc_executor_workers": (c_int32, [c_void_p]),
+    "psc_executor_set_values_version": (c_int32, [c_void_p, c_uint64]),
     "psc_executor_destroy": (None, [c_void_p]),
     "psc_bind": (c_int32, [c_void_p, c_void_p, POINTER(CsrView), c_int32, POINTER(c_void_p)]),
     "psc_bind_partitions": (

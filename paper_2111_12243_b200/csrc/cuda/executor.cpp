@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -122,11 +123,14 @@ struct psc_bound {
     int max_block_halo = -1;
     bool tiled = false;     // blocks grown over the unit graph (not row ranges)
     bool rec_dirty = true;  // values changed since the records were packed
+    uint64_t values_version = 0;  // run_* cache: caller's tag of the values on the device (0: none)
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
     DevBuf naive_ticket;    // psc_csr_sptrsv_device
     // overlapped upload of b (host path, record kernel): copy stream, chunk flags
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_before = nullptr, ev_copied = nullptr;
+    std::mutex host_mu;                  // the host-buffer entry points (host_call)
+    cudaEvent_t ev_host_done = nullptr;  // end of the last host-buffer call's work
     cudaEvent_t ev_part[kMaxSplitPasses] = {};  // host path, column split: x range q landed
     static constexpr int kYSlices = 4;             // ... and the last pass in row slices, y of each sent down at once
     int32_t ysl_row[kYSlices + 1] = {}, ysl_item[kYSlices + 1] = {}, ysl_long[kYSlices + 1] = {};
@@ -139,6 +143,7 @@ struct psc_bound {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (ev_before) cudaEventDestroy(ev_before);
         if (ev_copied) cudaEventDestroy(ev_copied);
+        if (ev_host_done) cudaEventDestroy(ev_host_done);
         for (cudaEvent_t e : ev_part)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_slice)
@@ -192,6 +197,9 @@ struct psc_executor {
     static constexpr size_t kCacheCap = 8;
     uint64_t clock = 0;
     DevBuf vx, vy, vb, vacc;
+    // psc_executor_set_values_version: the caller's tag for the matrix values
+    // the next run_* / execute_plan calls pass (0: unknown -- always upload)
+    uint64_t values_version = 0;
 };
 
 namespace pscb {
@@ -435,7 +443,12 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 // (by default only once x outgrows ~100 MB of the L2; a set PSC_FAST_SPLIT_BYTES always applies)
                 int parts = part_bytes > 0 && (v || xb > 100000000LL) ? static_cast<int>((xb + part_bytes - 1) / part_bytes) : 1;
                 parts = std::max(1, std::min(kMaxSplitPasses, parts));
-                build_fast(b.get(), a, ro, parts, s);
+                // one pass over rows of <= 16 entries: the thread-per-row kernel below is
+                // faster (one launch, no carries; config 1: 20.7 vs 23.6 us) and exact anyway
+                int32_t mx = 0;
+                for (int32_t r = L.row_begin; r < L.row_end && mx <= 16; ++r)
+                    mx = std::max(mx, static_cast<int32_t>(a.row_offsets[r + 1] - a.row_offsets[r]));
+                if (parts > 1 || mx > 16 || v) build_fast(b.get(), a, ro, parts, s);
             } else if (allow_split && L.simple && L.row_begin == 0 && L.row_end == a.n_rows) {
                 const char* v = std::getenv("PSC_SPMV_SPLIT_BYTES");
                 const int64_t min_bytes = v ? std::atoll(v) : 128000000LL;
@@ -988,7 +1001,7 @@ PSC_API psc_status psc_bound_sptrsv(psc_bound* b, const double* rhs, double* x, 
 // Host-buffer variants (the e2e path): H2D of the input, the kernel and the
 // D2H of the result, all enqueued on `stream`. Host memory should be pinned
 // for the copies to be asynchronous.
-PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x, double* y, void* stream) {
+static psc_status spmv_host_unlocked(psc_bound* b, const double* x, double* y, void* stream) {
     return guarded([&] {
         require(b && x && y, "spmv_host: null argument");
         require(b->kernel == PSC_KERNEL_SPMV, "run_spmv: plan was built for another kernel");
@@ -1090,7 +1103,7 @@ static int gather_ctas(int n_sms, int n_blocks) {
     return forced > 0 ? forced : std::max(8, n_sms - n_blocks);
 }
 
-PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double* x, double* acc, void* stream) {
+static psc_status sptrsv_host_unlocked(psc_bound* b, const double* rhs, double* x, double* acc, void* stream) {
     return guarded([&] {
         require(b && rhs && x, "sptrsv_host: null argument");
         require(b->kernel == PSC_KERNEL_SPTRSV, "run_sptrsv: plan was built for another kernel");
@@ -1168,6 +1181,34 @@ PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double
         if (acc) ck(cudaMemcpyAsync(acc, b->hacc.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
     });
 }
+// The host-buffer entry points share the bound's scratch buffers, copy
+// stream and events: calls on one bound -- from any thread, on any stream --
+// are serialised (each enqueues after the previous call's work).
+static psc_status host_call(psc_bound* b, void* stream, const std::function<psc_status()>& call) {
+    if (!b) return call();  // reports the null argument
+    std::lock_guard<std::mutex> lk(b->host_mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const psc_status pre = guarded([&] {
+        use_device(b->device);
+        if (b->ev_host_done) ck(cudaStreamWaitEvent(s, b->ev_host_done, 0), "wait");
+    });
+    if (pre != PSC_OK) return pre;
+    const psc_status st = call();
+    if (st != PSC_OK) return st;
+    return guarded([&] {
+        if (!b->ev_host_done) ck(cudaEventCreateWithFlags(&b->ev_host_done, cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(b->ev_host_done, s), "event");
+    });
+}
+
+PSC_API psc_status psc_bound_spmv_host(psc_bound* b, const double* x, double* y, void* stream) {
+    return host_call(b, stream, [&] { return spmv_host_unlocked(b, x, y, stream); });
+}
+
+PSC_API psc_status psc_bound_sptrsv_host(psc_bound* b, const double* rhs, double* x, double* acc, void* stream) {
+    return host_call(b, stream, [&] { return sptrsv_host_unlocked(b, rhs, x, acc, stream); });
+}
+
 // Diagnostics: copies the per-row publish times of the last solve (ns,
 // %globaltimer) followed by one arm time per block; needs PSC_TRSV_TRACE=1
 // at bind time. Returns the number of entries copied.
@@ -1232,6 +1273,24 @@ PSC_API psc_status psc_csr_sptrsv_device(psc_bound* b, const double* rhs, double
     });
 }
 
+// The run_* / execute_plan calls read the matrix values live, as the
+// reference does (upload on every call), unless the caller tagged them with a
+// version (psc_executor_set_values_version) equal to the one on the device.
+void upload_values(psc_executor* e, psc_bound* b, const double* values, cudaStream_t s) {
+    if (e->values_version != 0 && b->values_version == e->values_version) return;
+    b->val.upload_raw(values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);
+    b->rec_dirty = true;
+    b->values_version = e->values_version;
+}
+
+PSC_API psc_status psc_executor_set_values_version(psc_executor* e, uint64_t version) {
+    return guarded([&] {
+        require(e != nullptr, "set_values_version: null executor");
+        std::lock_guard<std::mutex> lk(e->mu);
+        e->values_version = version;
+    });
+}
+
 // run_spmv, executor.cpp:274-288.
 PSC_API psc_status psc_run_spmv(psc_executor* e, const psc_plan* plan, const psc_csr_view* a, const double* x,
                                 int64_t nx, double* y, int64_t ny) {
@@ -1243,7 +1302,7 @@ PSC_API psc_status psc_run_spmv(psc_executor* e, const psc_plan* plan, const psc
         psc_bound* b = cached_bound(e, plan, *a, false);
         cudaStream_t s = e->stream;
         use_device(e->device);
-        b->val.upload_raw(a->values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);  // values may change
+        upload_values(e, b, a->values, s);  // the reference reads values live
         e->vx.upload_raw(x, nx * sizeof(double), s);
         e->vy.ensure(std::max<int64_t>(ny, 1) * sizeof(double));
         bound_spmv(b, e->vx.as<double>(), e->vy.as<double>(), s);
@@ -1265,8 +1324,7 @@ PSC_API psc_status psc_run_sptrsv(psc_executor* e, const psc_plan* plan, const p
         psc_bound* b = cached_bound(e, plan, *l, false);
         cudaStream_t s = e->stream;
         use_device(e->device);
-        b->val.upload_raw(l->values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);
-        b->rec_dirty = true;
+        upload_values(e, b, l->values, s);
         size_t bytes = std::max<int64_t>(n, 1) * sizeof(double);
         e->vb.upload_raw(rhs, n * sizeof(double), s);
         e->vx.ensure(bytes);
@@ -1294,8 +1352,11 @@ PSC_API psc_status psc_execute_plan(psc_executor* e, const psc_plan* plan, const
         cudaStream_t s = e->stream;
         use_device(e->device);
         const int64_t n = a->n_rows, nc = a->n_cols;
-        b->val.upload_raw(ctx->matrix_values, a->nnz * sizeof(double), s);
-        b->rec_dirty = true;
+        if (!(e->values_version != 0 && b->values_version == e->values_version)) {
+            b->val.upload_raw(ctx->matrix_values, a->nnz * sizeof(double), s);
+            b->rec_dirty = true;
+            b->values_version = e->values_version;
+        }
         e->vy.upload_raw(ctx->accum, n * sizeof(double), s);
         if (solve) {
             // gather aliases solution (executor.hpp:12-23)

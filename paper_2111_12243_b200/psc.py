@@ -675,6 +675,11 @@ class Executor:
     def workers(self) -> int:
         return int(_capi.lib().psc_executor_workers(self._h))
 
+    def set_values_version(self, version: int) -> None:
+        """Tag the matrix values of the following run_* calls (0: unknown, always
+        upload them; a nonzero tag equal to the bound plan's skips the upload)."""
+        _check(_capi.lib().psc_executor_set_values_version(self._h, int(version)))
+
     @property
     def handle(self):
         return self._h

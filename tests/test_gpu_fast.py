@@ -64,7 +64,7 @@ def test_acceptance_suite_fast(exe):
         x = suite_input(kernel, a, ints)
         want = Oracle.spmv_baseline(a.view(), x)
         for per in (4, 8):
-            b, _ = fast_bound(exe, a, per=per)
+            b, _ = fast_bound(exe, a, split_bytes=-1, per=per)  # (set: the entry streams even for short rows)
             got = multiply(b, x)
             n_fast += b.info()["path"] == 2
             if ints:
@@ -76,10 +76,16 @@ def test_acceptance_suite_fast(exe):
 
 @pytest.mark.parametrize("config,scale", [(1, 1.0), (1, 0.01), (5, 0.02), (5, 0.2)])
 def test_configs_fast(exe, config, scale):
+    """Config 5: the flagged entry streams; config 1 (rows of <= 16 entries, one
+    pass): the thread-per-row kernel, which is faster there and bitwise the
+    parity result."""
     a = P.generate_config(config, scale)
     x = P.uniform_vector(a.n_cols, 10 + config)
-    b, _ = fast_bound(exe, a)
-    assert b.info()["path"] == 2
+    b, plan = fast_bound(exe, a)
+    assert b.info()["path"] == (0 if config == 1 else 2)
+    if config == 1:
+        assert np.array_equal(multiply(b, x).view(np.int64),
+                              Oracle.run_spmv(plan.export_arrays(), a.view(), x).view(np.int64))
     got = multiply(b, x)
     assert normwise_err(got, Oracle.spmv_baseline(a.view(), x)) <= 1e-12
     assert np.array_equal(got.view(np.int64), multiply(b, x).view(np.int64))  # deterministic

@@ -431,3 +431,29 @@ def test_device_inspector_configs(config, scale, kernel):
     assert dev.hash() == host.hash()
     assert dev.counts().n_codelets == host.counts().n_codelets
     assert dev.totals() == host.totals()
+
+
+@pytest.mark.parametrize("kernel", [KernelKind.Spmv, KernelKind.Sptrsv])
+def test_values_version_skips_reupload(kernel):
+    """psc_executor_set_values_version: untagged calls read the values live (as
+    the reference does); a call tagged with the version already on the device
+    keeps those values; a new tag uploads again."""
+    exe = P.Executor(1)
+    a = P.generate_config(2 if kernel == KernelKind.Sptrsv else 1, 0.02)
+    plan = P.inspect(kernel, a, 3, 8)
+    v = P.uniform_vector(a.n_rows, 3)
+    first = run_gpu(exe, plan, kernel, a, v)
+    assert bitwise_equal(first, run_oracle(plan, kernel, a, v))
+    a.values[:] *= 0.5  # in place, same arrays
+    live = run_gpu(exe, plan, kernel, a, v)
+    assert bitwise_equal(live, run_oracle(plan, kernel, a, v))  # untagged: re-uploaded
+    exe.set_values_version(7)
+    tagged = run_gpu(exe, plan, kernel, a, v)  # first call with tag 7 uploads
+    assert bitwise_equal(tagged, live)
+    a.values[:] *= 2.0
+    kept = run_gpu(exe, plan, kernel, a, v)  # same tag: the device keeps the halved values
+    assert bitwise_equal(kept, live)
+    exe.set_values_version(8)
+    again = run_gpu(exe, plan, kernel, a, v)
+    assert bitwise_equal(again, first)
+    exe.close()
