@@ -82,7 +82,7 @@ def config_dict(args, kernel, workload, n, nnz, world):
     sharded = kernel == "spmv" and world > 1
     return {"workload": workload, "kernel": kernel, "n": n, "nnz": nnz, "t": args.t, "groups": args.groups,
             "scale": args.scale, "mode": args.mode if kernel == "spmv" else "parity",
-            "parallelism": (f"row shards x{world} (x all-gather per step)" if sharded else
+            "parallelism": (f"row shards x{world} (x exchanged every step)" if sharded else
                             (f"replicas x{world}" if world > 1 else "single device")),
             "l2": "flushed before every timed step (2x-L2 write, then 2x-L2 read of a second buffer)"}
 
@@ -316,15 +316,41 @@ def run_ours(args):
     out = torch.empty(max(rows, 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
+    exchange = None
     if sharded:
-        # every rank owns the x slice of its rows; a step all-gathers x (NCCL), then multiplies
-        from paper_2111_12243_b200.dist import XExchange, shard_row_ranges
+        # every rank owns the x slice of its rows. A step exchanges x and
+        # multiplies: over peer memory (IPC windows; fast mode: copy-engine pulls
+        # pass by pass, each pass waiting only for its column range), or, where
+        # IPC is unavailable on any rank, an NCCL all-gather then the multiply
+        from paper_2111_12243_b200.dist import PeerExchange, XExchange, shard_row_ranges
 
-        xex = XExchange(shard_row_ranges(plan, world), a.n_cols, dev)
+        ranges = shard_row_ranges(plan, world)
         x_mine = vec[bound.row_begin:bound.row_end].clone()
+        pex, ok = None, 1
+        try:
+            pex = PeerExchange(bound, ranges, rank, a.n_cols)
+        except Exception as err:  # every rank reaches the all-reduce below
+            print(f"bench.py: peer exchange unavailable on rank {rank}: {err}", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and pex is not None:
+            pex.close()
+            pex = None
+        if pex is not None:
+            exchange = "peer pulls over NVLink (IPC windows)"
 
-        def step(b=bound):
-            b.spmv(xex.exchange(x_mine), out)
+            def exchange_multiply(xs):
+                pex.multiply(xs, out)
+        else:
+            exchange = "NCCL all-gather"
+            xex = XExchange(ranges, a.n_cols, dev)
+
+            def exchange_multiply(xs):
+                bound.spmv(xex.exchange(xs), out)
+
+        def step():
+            exchange_multiply(x_mine)
     elif kernel == "spmv":
         def step(b=bound):
             b.spmv(vec, out)
@@ -394,7 +420,7 @@ def run_ours(args):
 
         def e2e_step():
             dev_in.copy_(host_in, non_blocking=True)
-            bound.spmv(xex.exchange(dev_in), out)
+            exchange_multiply(dev_in)
             host_out.copy_(out, non_blocking=True)
 
         e2e_ms, _, _ = timed(e2e_step, args.steps, args.warmup, True)
@@ -469,8 +495,11 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": total_flops * (1 if sharded else world) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                "path": "psc_bound_*_host with pinned host buffers (the C ABI's host-buffer entry points)",
+                "path": ("per rank: its x slice up from pinned host memory, the exchange and the shard's multiply, "
+                         "its rows back down" if sharded else
+                         "psc_bound_*_host with pinned host buffers (the C ABI's host-buffer entry points)"),
                 "check": e2e_check},
+        "exchange": exchange,
         "gpu_launches": args.steps * bound.launches(),
         "clocks": sampler.summary(wall0, wall1),
         "inspector_seconds": inspector_s,

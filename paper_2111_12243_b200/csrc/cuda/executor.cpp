@@ -900,6 +900,44 @@ PSC_API psc_status psc_bound_spmv_peers(psc_bound* b, const psc_peer_window* pee
         require(expect == b->n_cols, "spmv_peers: peer windows must cover all columns");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         use_device(b->device);
+        if (b->canonical && b->fast_passes) {
+            // fast mode: the copy engines pull the remote runs pass by pass (each
+            // pass's column range, split by owner) on the copy stream, and every
+            // pass waits only for its own range -- the pulls of later ranges
+            // overlap the earlier passes' multiplies and take no SMs
+            if (!b->copy_stream) {
+                ck(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&b->ev_before, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&b->ev_copied, cudaEventDisableTiming), "event");
+            }
+            ck(cudaEventRecord(b->ev_before, s), "event");  // the caller's writes of x_window are done
+            ck(cudaStreamWaitEvent(b->copy_stream, b->ev_before, 0), "wait");
+            for (int q = 0; q < b->fast_passes; ++q) {
+                const int32_t p0 = b->fp_c0[q], p1 = b->fp_c0[q + 1];
+                for (size_t i = 0; i + 1 < b->remote_runs.size(); i += 2) {
+                    int32_t c = std::max(b->remote_runs[i], p0);
+                    const int32_t c1 = std::min(b->remote_runs[i + 1], p1);
+                    int32_t o = 0;
+                    while (c < c1) {
+                        while (peers[o].row_end <= c) ++o;
+                        const int32_t e = std::min(c1, peers[o].row_end);
+                        if (peers[o].base != x_window)
+                            ck(cudaMemcpyAsync(x_window + c, peers[o].base + c, static_cast<size_t>(e - c) * sizeof(double),
+                                               cudaMemcpyDefault, b->copy_stream),
+                               "peer pull");
+                        c = e;
+                    }
+                }
+                if (!b->ev_part[q]) ck(cudaEventCreateWithFlags(&b->ev_part[q], cudaEventDisableTiming), "event");
+                ck(cudaEventRecord(b->ev_part[q], b->copy_stream), "event");
+            }
+            for (int q = 0; q < b->fast_passes; ++q) {
+                ck(cudaStreamWaitEvent(s, b->ev_part[q], 0), "wait");
+                fast_pass_launch(b, q, x_window, y, s);
+            }
+            ck(cudaGetLastError(), "spmv_peers launch");
+            return;
+        }
         std::vector<int64_t> sig;
         for (int32_t q = 0; q < n_peers; ++q)
             sig.insert(sig.end(), {reinterpret_cast<int64_t>(peers[q].base), peers[q].row_begin, peers[q].row_end});

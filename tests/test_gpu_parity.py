@@ -336,7 +336,7 @@ def test_sptrsv_value_update_repacks(exe):
     assert not bitwise_equal(first, second)
 
 
-def _ipc_worker(rank, world, port, q):
+def _ipc_worker(rank, world, port, q, mode=0):
     import os
 
     import torch
@@ -345,13 +345,15 @@ def _ipc_worker(rank, world, port, q):
     from paper_2111_12243_b200.dist import PeerExchange, shard_partitions, shard_row_ranges
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if mode == 1:
+        os.environ["PSC_FAST_SPLIT_BYTES"] = "400000"  # several column passes
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         a = P.generate_config(5, 0.005)
         plan = P.inspect(KernelKind.Spmv, a, 3, 8)
         p0, p1 = shard_partitions(plan.counts().n_partitions, world, rank)
-        bound = P.BoundPlan(P.Executor(1, 0), plan, a, partitions=(p0, p1))
+        bound = P.BoundPlan(P.Executor(1, 0), plan, a, mode=mode, partitions=(p0, p1))
         ranges = shard_row_ranges(plan, world)
         ex = PeerExchange(bound, ranges, rank, a.n_cols, device=torch.device("cpu"))
         x = torch.from_numpy(P.uniform_vector(a.n_cols, 31)).cuda()
@@ -362,6 +364,10 @@ def _ipc_worker(rank, world, port, q):
             ex.multiply(x[b:e].contiguous(), y)
             torch.cuda.synchronize()
             outs.append(y.cpu().numpy())
+        y = torch.empty(e - b, dtype=torch.float64, device="cuda")
+        bound.spmv(x, y)  # the shard's multiply on the whole x, for comparison
+        torch.cuda.synchronize()
+        outs.append(y.cpu().numpy())
         dist.barrier()
         ex.close()
         q.put((rank, outs))
@@ -369,11 +375,15 @@ def _ipc_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_exchange_real_ipc_two_processes():
+@pytest.mark.parametrize("mode", [0, 1])
+def test_peer_exchange_real_ipc_two_processes(mode):
     """Two processes on this GPU exchange real CUDA IPC windows (gloo for the
-    control plane) and multiply their shards through the fused launch; the
-    stitched result equals the oracle bitwise. The processes' kernels never
-    wait on each other (each waits only for its own pulls)."""
+    control plane) and multiply their shards through the fused launch (parity
+    mode) or copy-engine pulls per column pass (fast mode); parity: the
+    stitched result equals the oracle bitwise; fast: every shard equals its
+    multiply on the whole x bitwise, and the stitched result is within 1e-12
+    normwise of the reference baseline. The processes' kernels never wait on
+    each other (each waits only for its own pulls)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -385,7 +395,7 @@ def test_peer_exchange_real_ipc_two_processes():
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
@@ -394,10 +404,19 @@ def test_peer_exchange_real_ipc_two_processes():
         assert p.exitcode == 0
     a = P.generate_config(5, 0.005)
     plan = P.inspect(KernelKind.Spmv, a, 3, 8)
-    want = Oracle.run_spmv(plan.export_arrays(), a.view(), P.uniform_vector(a.n_cols, 31))
-    for it in range(2):
-        got = np.concatenate([res[r][it] for r in range(world)])
-        assert bitwise_equal(got, want)
+    x = P.uniform_vector(a.n_cols, 31)
+    if mode == 0:
+        want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+        for it in range(2):
+            got = np.concatenate([res[r][it] for r in range(world)])
+            assert bitwise_equal(got, want)
+    else:
+        from tests.helpers import normwise_err
+
+        for r in range(world):
+            assert bitwise_equal(res[r][0], res[r][2]) and bitwise_equal(res[r][1], res[r][2]), r
+        got = np.concatenate([res[r][0] for r in range(world)])
+        assert normwise_err(got, Oracle.spmv_baseline(a.view(), x)) <= 1e-12
 
 
 # ---- GPU inspector (psc_inspect_device): the same plans as the host inspector ----
@@ -457,3 +476,52 @@ def test_values_version_skips_reupload(kernel):
     again = run_gpu(exe, plan, kernel, a, v)
     assert bitwise_equal(again, first)
     exe.close()
+
+
+@pytest.mark.parametrize("split_bytes", ["-1", "500000"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_peer_exchange_fast_mode(monkeypatch, exe, split_bytes, world):
+    """Fast-mode shards (config 5's entry streams, one or several column
+    passes): psc_bound_spmv_peers pulls each pass's remote runs with the copy
+    engines and runs the pass after its own range landed. Every shard equals
+    its own multiply on the fully gathered x bitwise, twice in a row, and the
+    stitched result is within 1e-12 normwise of the reference baseline."""
+    import torch
+
+    from paper_2111_12243_b200.dist import shard_partitions
+    from tests.helpers import normwise_err
+
+    monkeypatch.setenv("PSC_FAST_SPLIT_BYTES", split_bytes)
+    a = P.generate_config(5, 0.01)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(a.n_cols, 23)
+    xt = torch.from_numpy(x).cuda()
+    n_parts = plan.counts().n_partitions
+    bounds, ranges = [], []
+    for r in range(world):
+        p0, p1 = shard_partitions(n_parts, world, r)
+        bounds.append(P.BoundPlan(exe, plan, a, mode=1, partitions=(p0, p1)))
+        ranges.append((bounds[-1].row_begin, bounds[-1].row_end))
+        assert bounds[-1].info()["path"] == 2
+    windows = []
+    for (b, e) in ranges:
+        w = torch.full((a.n_cols,), float("nan"), dtype=torch.float64, device="cuda")
+        w[b:e] = xt[b:e]
+        windows.append(w)
+    peers = [(windows[q].data_ptr(), b, e) for q, (b, e) in enumerate(ranges)]
+    ref = []
+    for q, bound in enumerate(bounds):
+        y = torch.empty(ranges[q][1] - ranges[q][0], dtype=torch.float64, device="cuda")
+        bound.spmv(xt, y)
+        ref.append(y)
+    for _ in range(2):
+        ys = []
+        for q, bound in enumerate(bounds):
+            y = torch.full((ranges[q][1] - ranges[q][0],), float("nan"), dtype=torch.float64, device="cuda")
+            bound.spmv_peers(peers, windows[q], y)
+            ys.append(y)
+        torch.cuda.synchronize()
+        for q in range(world):
+            assert bitwise_equal(ys[q].cpu().numpy(), ref[q].cpu().numpy()), q
+    got = torch.cat(ys).cpu().numpy()
+    assert normwise_err(got, Oracle.spmv_baseline(a.view(), x)) <= 1e-12
