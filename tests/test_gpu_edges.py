@@ -409,3 +409,54 @@ def test_run_cache_sees_in_place_structure_edits(exe):
         pytest.skip("edit would unsort the row")
     with pytest.raises((P.LogicError, P.InvalidArgument)):
         P.run_spmv(plan, a, x, y, exe)
+
+
+@pytest.mark.parametrize("kernel,config,mode", [(0, 5, 1), (1, 2, 0)])
+def test_host_buffer_calls_from_threads(kernel, config, mode):
+    """psc_bound_*_host calls on one bound from four host threads, each on its
+    own stream: the calls share the bound's scratch buffers and are
+    serialised, so every thread gets the right result."""
+    import threading
+
+    import torch
+
+    exe = P.Executor(1)
+    a = P.generate_config(config, 0.002 if config == 5 else 0.05)
+    kk = P.KernelKind.Spmv if kernel == 0 else P.KernelKind.Sptrsv
+    import os
+
+    if kernel == 0:
+        os.environ["PSC_FAST_SPLIT_BYTES"] = "100000"  # several column passes: copy stream + events
+    try:
+        plan = P.inspect(kk, a, 3, 8)
+        bound = P.BoundPlan(exe, plan, a, mode=mode)
+    finally:
+        os.environ.pop("PSC_FAST_SPLIT_BYTES", None)
+    vecs = [P.uniform_vector(a.n_cols, 40 + i) for i in range(4)]
+    want = []
+    for v in vecs:
+        out = np.empty(a.n_rows)
+        (bound.spmv_host if kernel == 0 else bound.sptrsv_host)(v, out)
+        torch.cuda.synchronize()
+        want.append(out)
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            for _ in range(5):
+                out = np.full(a.n_rows, np.nan)
+                (bound.spmv_host if kernel == 0 else bound.sptrsv_host)(vecs[i], out, stream=s)
+                s.synchronize()
+                if not np.array_equal(out.view(np.int64), want[i].view(np.int64)):
+                    errors.append(i)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    exe.close()
