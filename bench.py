@@ -291,13 +291,16 @@ def run_ours(args):
     kk = P.KernelKind.Spmv if kernel == "spmv" else P.KernelKind.Sptrsv
     a = P.generate_config(args.config, args.scale)
     t0 = time.perf_counter()
-    plan = P.inspect(kk, a, args.t, args.groups)
+    # (ranks share the host: each inspects with its share of the cores; the plan is the same)
+    plan = P.inspect(kk, a, args.t, args.groups, max(1, (os.cpu_count() or 1) // world) if world > 1 else 0)
     inspector_s = time.perf_counter() - t0
-    t0 = time.perf_counter()  # the same inspection with the window mining on the GPU (same plan, bit for bit)
-    plan_dev = P.inspect_device(kk, a, args.t, args.groups, local)
-    inspector_dev_s = time.perf_counter() - t0
-    inspector_dev_same = plan_dev.hash() == plan.hash()
-    del plan_dev
+    inspector_dev_s, inspector_dev_same = None, None
+    if world == 1:  # the same inspection with the window mining on the GPU (same plan, bit for bit)
+        t0 = time.perf_counter()
+        plan_dev = P.inspect_device(kk, a, args.t, args.groups, local)
+        inspector_dev_s = time.perf_counter() - t0
+        inspector_dev_same = plan_dev.hash() == plan.hash()
+        del plan_dev
     exe = P.Executor(1, local)
     n_parts = plan.counts().n_partitions
     sharded = kernel == "spmv" and world > 1
