@@ -520,7 +520,10 @@ def run_ours(args):
             "note": "each entry gathers one x value at a random column (config 5); the L1/L2 path serves ~1 such gather "
                     "per SM-cycle (tools/gather_probe.cu on this B200: 255 G gathers/s beside a 12 B/entry stream), "
                     "so 401M gathers take >= ~1.57 ms whatever the HBM bandwidth (DESIGN.md)",
-            "gathers_per_step": a.nnz()}
+            "gathers_per_step": a.nnz(),
+            "gathers_per_s_measured": 255e9,
+            "bound_ms": a.nnz() / 255e9 * 1e3,
+            "frac": (a.nnz() / 255e9 * 1e3) / ms_step}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
