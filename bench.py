@@ -515,7 +515,7 @@ def run_ours(args):
             "levels": n_parts, "ns_per_level": ms_step * 1e6 / max(1, n_parts),
             "note": "sync-free solve: time ~ levels x per-level hop latency"}
         line["roofline"]["record_pack"] = "the per-row record pack (trsv_pack_kernel) runs at bind and after a value change, outside the timed step"
-    if kernel == "spmv" and mode == "fast":
+    if args.config == 5 and mode == "fast":  # uniformly random columns: the gathers, not HBM, bound the step
         line["roofline"]["gather_bound"] = {
             "note": "each entry gathers one x value at a random column (config 5); the L1/L2 path serves ~1 such gather "
                     "per SM-cycle (tools/gather_probe.cu on this B200: 255 G gathers/s beside a 12 B/entry stream), "
