@@ -103,6 +103,11 @@ struct psc_bound {
     int64_t fl_n_ent[kMaxSplitPasses] = {};
     int fl_n_chunks[kMaxSplitPasses] = {};
     int fl_per = 4;  // entries per lane (PSC_FAST_PER: 4 or 8)
+    // the last pass's stream cut into row slices at chunks that start a row
+    // (no carry crosses a cut), so the host path sends each slice's y down
+    // while the next slice runs
+    static constexpr int kFastSlices = 8;
+    int32_t fsl_chunk[kFastSlices + 1] = {}, fsl_row[kFastSlices + 1] = {};
     bool chain_mode = false;
     int max_block_units = 0;
     DevBuf block_row, block_unit, unit_start;
@@ -134,7 +139,7 @@ struct psc_bound {
     cudaEvent_t ev_part[kMaxSplitPasses] = {};  // host path, column split: x range q landed
     static constexpr int kYSlices = 4;             // ... and the last pass in row slices, y of each sent down at once
     int32_t ysl_row[kYSlices + 1] = {}, ysl_item[kYSlices + 1] = {}, ysl_long[kYSlices + 1] = {};
-    cudaEvent_t ev_slice[kYSlices] = {};
+    cudaEvent_t ev_slice[kYSlices > kFastSlices ? kYSlices : kFastSlices] = {};
     DevBuf b_ready, g_order;  // host path: per-unit arrival flags (+ gather ticket), gather order
     int n_units_total = 0;
     int* flag_patterns = nullptr;  // pinned, immutable: [i] = 0x01010101 * i (flags are written by the copy engine)
@@ -349,6 +354,19 @@ void build_fast(psc_bound* b, const psc_csr_view& a, const std::vector<int32_t>&
                     while (r < n && fo[r + 1] <= c * ch) ++r;
                     m0[c] = r;
                 }
+            }
+            if (q == parts - 1) {  // y slices: cut at chunks whose first entry starts a row
+                int64_t cut = 0;
+                b->fsl_chunk[0] = 0;
+                b->fsl_row[0] = 0;
+                for (int i = 1; i < psc_bound::kFastSlices; ++i) {
+                    cut = std::max<int64_t>(cut, n_chunks * i / psc_bound::kFastSlices);
+                    while (cut < n_chunks && fo[m0[cut]] != cut * ch) ++cut;
+                    b->fsl_chunk[i] = static_cast<int32_t>(cut);
+                    b->fsl_row[i] = cut < n_chunks ? m0[cut] : n;
+                }
+                b->fsl_chunk[psc_bound::kFastSlices] = static_cast<int32_t>(n_chunks);
+                b->fsl_row[psc_bound::kFastSlices] = n;
             }
             b->fl_colf[q].upload(colf, s);
             b->fl_val[q].upload(pv, s);
@@ -1046,7 +1064,7 @@ static psc_status spmv_host_unlocked(psc_bound* b, const double* x, double* y, v
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         use_device(b->device);
         b->hy.ensure(std::max(1, b->rows()) * sizeof(double));
-        if (b->canonical && b->fast_passes > 1) {
+        if (b->canonical && b->fast_passes >= 1) {
             // fast column-split passes: x range q goes up on the copy stream and
             // pass q waits only for it, so the later ranges' upload hides the
             // earlier passes
@@ -1067,11 +1085,41 @@ static psc_status spmv_host_unlocked(psc_bound* b, const double* x, double* y, v
                                        cudaMemcpyHostToDevice, b->copy_stream), "H2D");
                 ck(cudaEventRecord(b->ev_part[q], b->copy_stream), "event");
             }
-            for (int q = 0; q < b->fast_passes; ++q) {
+            const int last = b->fast_passes - 1;
+            for (int q = 0; q < last; ++q) {
                 ck(cudaStreamWaitEvent(s, b->ev_part[q], 0), "wait");
                 fast_pass_launch(b, q, b->hx.as<double>(), b->hy.as<double>(), s);
             }
+            // the last pass slice by slice; each slice's y rows are final once it ran
+            ck(cudaStreamWaitEvent(s, b->ev_part[last], 0), "wait");
+            const FlagPassDev whole = flag_pass(b, last);
+            const int64_t ch = flag_chunk_entries(b->fl_per);
+            for (int i = 0; i < psc_bound::kFastSlices; ++i) {
+                const int32_t c0 = b->fsl_chunk[i], c1 = b->fsl_chunk[i + 1];
+                const int32_t r0 = b->fsl_row[i], r1 = b->fsl_row[i + 1];
+                if (c1 > c0) {
+                    FlagPassDev P = whole;
+                    P.colf += c0 * ch;
+                    P.val += c0 * ch;
+                    P.chunk_m0 += c0;
+                    P.carry_val += c0;
+                    P.carry_row += c0;
+                    P.n_chunks = c1 - c0;
+                    P.n_ent = c1 == whole.n_chunks ? whole.n_ent - c0 * ch : static_cast<int64_t>(c1 - c0) * ch;
+                    launch_spmv_flag(P, b->hx.as<double>(), b->hy.as<double>(), last > 0, b->n_sms, s);
+                }
+                if (r1 > r0) {
+                    if (!b->ev_slice[i]) ck(cudaEventCreateWithFlags(&b->ev_slice[i], cudaEventDisableTiming), "event");
+                    ck(cudaEventRecord(b->ev_slice[i], s), "event");
+                    ck(cudaStreamWaitEvent(b->copy_stream, b->ev_slice[i], 0), "wait");
+                    ck(cudaMemcpyAsync(y + r0, b->hy.as<double>() + r0, static_cast<size_t>(r1 - r0) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, b->copy_stream), "D2H");
+                }
+            }
+            ck(cudaEventRecord(b->ev_copied, b->copy_stream), "event");
+            ck(cudaStreamWaitEvent(s, b->ev_copied, 0), "wait");  // the caller's stream covers the copies
             ck(cudaGetLastError(), "spmv launch");
+            return;
         } else if (b->canonical && b->split) {
             // Column-split passes: pass q reads only x's column range q, so the
             // ranges go up on a copy stream one by one and pass q waits for its
