@@ -128,11 +128,6 @@ struct psc_bound {
     int max_block_halo = -1;
     bool tiled = false;     // blocks grown over the unit graph (not row ranges)
     bool rec_dirty = true;  // values changed since the records were packed
-    // wavefront record kernel (trsv_wave.cu): static warp schedules over the same blocks
-    bool wave = false;
-    bool wave_dirty = true;
-    DevBuf wstep_ptr, wave_row, wave_slot, wave_src, wave_rec;
-    int64_t wave_slots = 0;
     uint64_t values_version = 0;  // run_* cache: caller's tag of the values on the device (0: none)
     DevBuf hx, hy, hacc;    // scratch for the host-buffer entry points
     DevBuf naive_ticket;    // psc_csr_sptrsv_device
@@ -680,21 +675,6 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                 const int th = pick_threads(L, b->max_block_halo);
                 require(th > 0, "bind: solve block does not fit in shared memory");
                 b->trsv_threads = th;
-                // wavefront schedule (PSC_TRSV_WAVE=0: off; =1: also when idle slots outnumber the rows)
-                double blowup = 1.0;
-                if (const char* wv = std::getenv("PSC_TRSV_WAVE")) blowup = wv[0] == '0' ? -1.0 : (wv[0] == '1' ? 8.0 : 1.0);
-                if (blowup >= 0.0 && th >= 64 &&
-                    sptrsv_wave_smem_bytes(th, L.max_block_rows, b->max_block_halo) <= 232448 &&
-                    wave_schedule(L, a, th, 1.0 + blowup)) {
-                    b->wave = true;
-                    b->wave_slots = static_cast<int64_t>(L.wave_row.size());
-                    b->wstep_ptr.upload(L.wstep_ptr, s);
-                    b->wave_row.upload(L.wave_row, s);
-                    b->wave_slot.upload(L.wave_slot, s);
-                    b->wave_src.upload(L.wave_src, s);
-                    b->wave_rec.ensure(static_cast<size_t>(b->wave_slots) * trsv_rec_bytes());
-                    launch_trsv_wave_nulls(b->wave_row.as<int32_t>(), b->wave_slots, b->wave_rec.p, s);
-                }
             }
             b->max_block_rows = L.max_block_rows;
             b->ticket.ensure(2 * sizeof(int32_t));
@@ -785,29 +765,6 @@ void bound_sptrsv(psc_bound* b, const double* rhs, double* x, double* acc, cudaS
                             b->q_units.as<int32_t>(), b->chain_mode ? b->q_ends.as<int32_t>() : nullptr, b->n_q_units,
                             !b->chain_mode, b->segs(), b->q_next.as<int>(),
                             b->trace.as<unsigned long long>(), b->rows(), b->n_sms, b->q_backoff, s);
-    } else if (b->canonical && b->wave && !x_host) {
-        if (b->wave_dirty) {
-            launch_trsv_wave_pack(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), b->row_block.as<int32_t>(),
-                                  b->row_loc.as<int32_t>(), b->block_row.as<int32_t>(), b->halo_ptr.as<int32_t>(),
-                                  b->halo_key.as<int32_t>(), b->halo_pos.as<int32_t>(), b->wave_slot.as<int32_t>(),
-                                  b->wave_src.as<int32_t>(), b->rows(), b->wave_rec.p, s);
-            b->wave_dirty = false;
-        }
-        b->epoch = b->epoch == INT32_MAX ? 1 : b->epoch + 1;
-        static const int trace_rows = [] {
-            const char* tr = std::getenv("PSC_TRSV_TRACE_ROWS");
-            return tr && tr[0] == '0' ? 0 : 1;
-        }();
-        static const int poll_ns = [] {
-            const char* pn = std::getenv("PSC_TRSV_POLL_NS");
-            return pn ? std::atoi(pn) : 0;
-        }();
-        WaveArgs W{rhs, x, acc, b->block_row.as<int32_t>(), b->block_unit.as<int32_t>(), b->unit_start.as<int32_t>(),
-                   b->unit_len.as<int32_t>(), b->unit_loc.as<int32_t>(), b->halo_ptr.as<int32_t>(),
-                   b->halo_col.as<int32_t>(), b->wstep_ptr.as<int32_t>(), b->wave_row.as<int32_t>(), b->wave_rec.p,
-                   b->ticket.as<int32_t>(), b->armed.as<int32_t>(), b->trace.as<unsigned long long>(), b->epoch,
-                   b->max_block_rows, b->max_block_halo, b->n_blocks, poll_ns, trace_rows};
-        launch_sptrsv_wave(W, b->trsv_threads, s);
     } else if (b->canonical) {
         if (b->trsv_lean == 2 && b->rec_dirty) {
             launch_trsv_pack(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), b->row_block.as<int32_t>(),
@@ -1409,7 +1366,6 @@ void upload_values(psc_executor* e, psc_bound* b, const double* values, cudaStre
     if (e->values_version != 0 && b->values_version == e->values_version) return;
     b->val.upload_raw(values + b->k_begin, (b->k_end - b->k_begin) * sizeof(double), s);
     b->rec_dirty = true;
-    b->wave_dirty = true;
     b->values_version = e->values_version;
 }
 
@@ -1485,7 +1441,6 @@ PSC_API psc_status psc_execute_plan(psc_executor* e, const psc_plan* plan, const
         if (!(e->values_version != 0 && b->values_version == e->values_version)) {
             b->val.upload_raw(ctx->matrix_values, a->nnz * sizeof(double), s);
             b->rec_dirty = true;
-            b->wave_dirty = true;
             b->values_version = e->values_version;
         }
         e->vy.upload_raw(ctx->accum, n * sizeof(double), s);

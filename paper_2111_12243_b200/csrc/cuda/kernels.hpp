@@ -130,38 +130,6 @@ size_t trsv_rec_bytes();
 void launch_trsv_pack(const int32_t* ro, const int32_t* col, const double* val, const int32_t* row_block,
                       const int32_t* row_loc, const int32_t* block_row, const int32_t* halo_ptr, const int32_t* halo_key,
                       const int32_t* halo_pos, int n_rows, void* rec, cudaStream_t stream);
-// Wavefront record solve (trsv_wave.cu): the record kernel's blocks, unit
-// tables and halos, every solving warp walking the static schedule of
-// lower.cpp wave_schedule (wstep_ptr: step ranges per (block, warp); srow: 32
-// row slots per step; rec: 2048 bytes per step, four 16-byte chunk planes).
-struct WaveArgs {
-    const double* b;
-    double* x;
-    double* acc_out;
-    const int32_t* block_row;
-    const int32_t* block_unit;
-    const int32_t* unit_start;
-    const int32_t* unit_len;
-    const int32_t* unit_loc;
-    const int32_t* halo_ptr;
-    const int32_t* halo_col;
-    const int32_t* wstep_ptr;
-    const int32_t* srow;
-    const void* rec;
-    int32_t* ticket;
-    int32_t* armed;
-    unsigned long long* trace;
-    int epoch, max_rows, max_halo, n_blocks;
-    int poll_ns;     // sleep between polls of a missing operand
-    int trace_rows;  // diagnostics: per-row publish times (0: only the loop counters)
-};
-void launch_sptrsv_wave(const WaveArgs& A, int threads, cudaStream_t stream);
-void launch_trsv_wave_pack(const int32_t* ro, const int32_t* col, const double* val, const int32_t* row_block,
-                           const int32_t* row_loc, const int32_t* block_row, const int32_t* halo_ptr,
-                           const int32_t* halo_key, const int32_t* halo_pos, const int32_t* wslot, const int32_t* wsrc,
-                           int n_rows, void* rec, cudaStream_t stream);
-void launch_trsv_wave_nulls(const int32_t* srow, int64_t n_slots, void* rec, cudaStream_t stream);
-size_t sptrsv_wave_smem_bytes(int threads, int max_rows, int max_halo);
 // mismatches between the record kernel's division and __ddiv_rn on n random operand pairs (-1: CUDA error)
 int64_t division_selftest(uint64_t seed, int64_t n, int exp_span);
 size_t sptrsv_smem_bytes(int threads, int max_rows, int max_units, int max_halo);  // record kernel

@@ -613,98 +613,6 @@ bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows) {
     return true;
 }
 
-bool wave_schedule(Lowered& L, const psc_csr_view& a, int threads, double max_blowup) {
-    const int32_t nb = static_cast<int32_t>(L.block_row.size()) - 1;
-    const int32_t nr = L.row_end - L.row_begin;
-    const int nw = threads / 32;
-    if (nb <= 0 || nw <= 0 || L.row_block.empty()) return false;
-    std::vector<int32_t> g(nr, -1);  // simulated step of every row within its block
-    std::vector<int32_t> wstep_ptr{0}, wave_row, wave_slot(nr, -1);
-    const int64_t slot_cap = static_cast<int64_t>(max_blowup * nr) + 32LL * nw * nb + 1024;
-    struct Cursor {
-        int32_t u, j;  // unit (block-local index), row within it
-    };
-    std::vector<Cursor> cur(threads);
-    std::vector<std::vector<std::pair<int32_t, int32_t>>> warp_rows(nw);  // (step, row) per warp
-    for (int32_t bi = 0; bi < nb; ++bi) {
-        const int32_t U0 = L.block_unit[bi], nU = L.block_unit[bi + 1] - U0;
-        int64_t remaining = 0;
-        for (int32_t u = 0; u < nU; ++u) remaining += L.unit_len[U0 + u];
-        for (int l = 0; l < threads; ++l) cur[l] = {l, 0};
-        for (auto& v : warp_rows) v.clear();
-        int32_t t = 0;
-        while (remaining > 0) {
-            bool moved = false;
-            for (int l = 0; l < threads; ++l) {
-                Cursor& c = cur[l];
-                if (c.u >= nU) continue;
-                const int32_t r = L.unit_start[U0 + c.u] + c.j;  // local row
-                const int32_t gr = r + L.row_begin;
-                bool ok = true;
-                for (int64_t k = a.row_offsets[gr]; k < a.row_offsets[gr + 1] - 1 && ok; ++k) {
-                    const int32_t cc = a.col_indices[k] - L.row_begin;
-                    if (cc < 0 || L.row_block[cc] != bi) continue;  // halo: polled at run time
-                    ok = g[cc] >= 0 && g[cc] < t;
-                }
-                if (!ok) continue;
-                g[r] = t;
-                warp_rows[l >> 5].push_back({t, r});
-                wave_slot[r] = l & 31;  // lane for now
-                moved = true;
-                --remaining;
-                if (++c.j == L.unit_len[U0 + c.u]) {
-                    c.u += threads;
-                    c.j = 0;
-                }
-            }
-            if (!moved) return false;  // not reachable for topologically ordered units
-            ++t;
-        }
-        for (int w = 0; w < nw; ++w) {
-            auto& rows = warp_rows[w];  // already in step order (rounds ascend)
-            int32_t base = wstep_ptr.back(), steps = 0, last = -1;
-            for (auto& e : rows) {
-                if (e.first != last) {
-                    last = e.first;
-                    ++steps;
-                    wave_row.resize(static_cast<size_t>(base + steps) * 32, -1);
-                }
-                const int64_t slot = static_cast<int64_t>(base + steps - 1) * 32 + wave_slot[e.second];
-                wave_row[slot] = e.second;
-                wave_slot[e.second] = static_cast<int32_t>(slot);
-            }
-            wstep_ptr.push_back(base + steps);
-            if (static_cast<int64_t>(wave_row.size()) > slot_cap) return false;
-        }
-    }
-    if (static_cast<int64_t>(wave_row.size()) > 0x7FFFFFFFLL) return false;
-    // operands produced by the row's own warp in the step before the row's: taken from the
-    // producing lane's register (steps of one warp are consecutive slot ranges)
-    std::vector<int32_t> wave_src(nr, -1);
-    std::vector<int32_t> step_warp(wave_row.size() / 32, 0);
-    for (size_t wi = 0; wi + 1 < wstep_ptr.size(); ++wi)
-        for (int32_t st = wstep_ptr[wi]; st < wstep_ptr[wi + 1]; ++st) step_warp[st] = static_cast<int32_t>(wi);
-    for (int32_t r = 0; r < nr; ++r) {
-        const int32_t gr = r + L.row_begin;
-        const int32_t my = wave_slot[r] >> 5;
-        const int64_t k0 = a.row_offsets[gr], kd = a.row_offsets[gr + 1] - 1;
-        uint32_t src = 0xFFFFFFFFu;
-        for (int64_t k = k0; k < kd && k - k0 < 4; ++k) {
-            const int32_t cc = a.col_indices[k] - L.row_begin;
-            if (cc < 0 || L.row_block[cc] != L.row_block[r]) continue;
-            const int32_t ps = wave_slot[cc];
-            if (my > 0 && (ps >> 5) == my - 1 && step_warp[my - 1] == step_warp[my])
-                src = (src & ~(0xFFu << (8 * (k - k0)))) | (static_cast<uint32_t>(ps & 31) << (8 * (k - k0)));
-        }
-        wave_src[r] = static_cast<int32_t>(src);
-    }
-    L.wave_src = std::move(wave_src);
-    L.wstep_ptr = std::move(wstep_ptr);
-    L.wave_row = std::move(wave_row);
-    L.wave_slot = std::move(wave_slot);
-    return true;
-}
-
 void block_halos(Lowered& L, const psc_csr_view& a) {
     const int32_t nb = static_cast<int32_t>(L.block_row.size()) - 1;
     const int32_t nr = L.row_end - L.row_begin;

@@ -72,12 +72,6 @@ struct Lowered {
     std::vector<int32_t> halo_ptr, halo_col;  // halo_col: in production (level) order
     std::vector<int32_t> halo_key, halo_pos;  // the same columns sorted, and their halo_col positions
     int32_t max_block_halo = 0;
-    // wavefront record kernel (wave_schedule): per (block, warp) the range of
-    // its steps, every slot's row (32 per step, -1: idle), every row's slot
-    std::vector<int32_t> wstep_ptr, wave_row, wave_slot;
-    // per row, four bytes: operand j is the last x of that lane of the row's warp (the row's
-    // column was solved in the warp's previous step), or -1
-    std::vector<int32_t> wave_src;
     std::string why_general;  // reason the plan is not canonical
 
     // general interpreter tables (only when !canonical)
@@ -119,14 +113,6 @@ bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows);
 // Fill halo_ptr / halo_col / max_block_halo from row_block (after unit_maps
 // or tile_chain_blocks).
 void block_halos(Lowered& L, const psc_csr_view& a);
-
-// Static schedule of the wavefront record kernel (trsv_wave.cu) for CTAs of
-// `threads` solving lanes (unit i of a block on lane i % threads): the block
-// is simulated in lockstep -- step g takes, from every lane, its next row once
-// the row's in-block operands finished at steps < g -- and a warp's schedule
-// lists the steps in which one of its lanes has a row. Returns false (L
-// untouched) when the idle slots would exceed max_blowup x the rows.
-bool wave_schedule(Lowered& L, const psc_csr_view& a, int threads, double max_blowup);
 
 // General-path lowering of a plan with explicit tables (imported with
 // psc_plan_from_arrays: the reference's own CodeletPlan) without a matrix:

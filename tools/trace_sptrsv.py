@@ -27,13 +27,11 @@ for _ in range(3):
 torch.cuda.synchronize()
 n = a.n_rows
 nb = info["work_units"]
-buf = np.zeros(n + nb + 16, dtype=np.uint64)
+buf = np.zeros(n + nb + 8, dtype=np.uint64)
 got = _capi.lib().psc_bound_trace(bound._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size)
-assert got >= n + nb + 8, got
-stats = buf[n + nb:n + nb + 4].astype(np.float64); st = buf[n + nb:n + nb + 8 + 8].astype(np.float64) if buf.size >= n + nb + 16 else None; buf = buf[:n + nb]
+assert got == n + nb + 8, got
+stats = buf[n + nb:n + nb + 4].astype(np.float64); buf = buf[:n + nb]
 rounds = stats[0]
-if st is not None and st[3] > 0:
-    print(f'wave: steps {st[3]:.0f} wait cyc/step {st[4]/st[3]:.0f} poll cyc/step {st[5]/st[3]:.0f}; block0 warp0: steps {st[7]:.0f} cyc/step {st[6]/max(st[7],1):.0f} wait {st[8]/max(st[7],1):.0f} poll {st[9]/max(st[7],1):.0f} polls {st[10]:.0f} fp {st[11]/max(st[7],1):.0f} store {st[12]/max(st[7],1):.0f}')
 print(f'warps {stats[2]:.0f} rounds/warp {stats[0]/max(stats[2],1):.0f} cycles/round {stats[1]/max(stats[0],1):.0f} rows {stats[3]:.0f} (3 solves accumulated)')
 t_rows = buf[:n].astype(np.int64)
 t_arm = buf[n:].astype(np.int64)
@@ -48,7 +46,7 @@ for r in range(n):
     if k1 > k0:
         level[r] = level[ci[k0:k1]].max() + 1
 L = level.max() + 1
-print(f"n={n} levels={L} blocks={nb} block_rows={info.get('max_block_rows', 10000)}")
+print(f"n={n} levels={L} blocks={nb} block_rows={info.get('max_block_rows', info.get('passes_or_block_rows', 10000))}")
 print(f"arm times (us): min {t_arm.min()/1e3:.1f} max {t_arm.max()/1e3:.1f}")
 print(f"total (last publish) {t_rows.max()/1e3:.1f} us; warp rounds (sum over warps, 3 solves) {rounds}")
 lv_max = np.zeros(L)
@@ -58,7 +56,7 @@ step = np.diff(lv_max)
 print("per-level finish (us) at levels 0,10,50,100,150,200,250,last:",
       [round(lv_max[i] / 1e3, 1) for i in (0, 10, 50, 100, 150, 200, 250, L - 1) if i < L])
 print(f"per-level step: median {np.median(step)/1e3:.2f} us, mean {step.mean()/1e3:.2f} us, max {step.max()/1e3:.1f} us")
-blk = np.arange(n) // info.get("max_block_rows", 10000)
+blk = np.arange(n) // info.get("max_block_rows", info.get("passes_or_block_rows", 10000))
 for k in list(range(0, nb, max(1, nb // 8)))[:10]:
     m = blk == k
     print(f"block {k}: rows finish {t_rows[m].min()/1e3:.1f}..{t_rows[m].max()/1e3:.1f} us, levels {level[m].min()}..{level[m].max()}")
