@@ -225,7 +225,8 @@ PSC_API int64_t psc_bound_trace(const psc_bound* b, uint64_t* out, int64_t cap);
 /* Number of kernel launches one psc_bound_* call enqueues. */
 PSC_API int32_t psc_bound_launches(const psc_bound* b);
 /* Lowering diagnostics, out[0..7]: rows, segments (0 = every row is one
- * implicit full-row segment), work units (SpMV chunks / SpTRSV row blocks),
+ * implicit full-row segment), work units (SpMV chunks, or the warp items of
+ * the shifted-run kernel when it is in use / SpTRSV row blocks),
  * path (0 parity kernels, 1 general interpreter, 2 fast-mode SpMV),
  * algorithmic bytes per call, device bytes held, long rows,
  * column passes (SpMV; 0 = one pass over all of x) / max block rows (SpTRSV). */

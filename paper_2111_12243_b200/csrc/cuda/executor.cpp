@@ -77,6 +77,8 @@ struct psc_bound {
     int n_chunks = 0, n_blocks = 0, max_block_rows = 0, n_sms = 148;
     int64_t n_segments = 0, long_rows = 0;
     int spmv_short = 0;  // > 0: every row holds <= spmv_short entries (thread-per-row SpMV)
+    DevBuf run_items;    // spmv_short: warp items over shifted runs (spmv_run_kernel); empty: spmv_row_kernel
+    int n_run_items = 0;
     // fused x exchange (sharded simple SpMV): remote column runs and per-work flags
     bool peer_ok = false;
     std::vector<int32_t> remote_runs;  // [c0, c1) pairs of columns outside the shard's rows
@@ -488,6 +490,17 @@ std::unique_ptr<psc_bound> make_bound(int device, const Plan& p, const psc_csr_v
                     mx = std::max(mx, static_cast<int32_t>(a.row_offsets[r + 1] - a.row_offsets[r]));
                 b->spmv_short = mx <= 16 ? std::max<int32_t>(mx, 1) : 0;
                 if (const char* rk = std::getenv("PSC_SPMV_ROWK"); rk && rk[0] == '0') b->spmv_short = 0;
+                // shifted runs (stencil interiors): rows without row offsets or column loads, when
+                // they cover most of the matrix (PSC_SPMV_RUNS=0 disables)
+                const char* rv = std::getenv("PSC_SPMV_RUNS");
+                if (b->spmv_short > 0 && !(rv && rv[0] == '0')) {
+                    std::vector<int32_t> items;
+                    const int64_t in_runs = build_run_items(L, a, items);
+                    if (2 * in_runs >= static_cast<int64_t>(L.row_end - L.row_begin) && !items.empty()) {
+                        b->run_items.upload(items, s);
+                        b->n_run_items = static_cast<int>(items.size() / 20);
+                    }
+                }
             }
             // a shard of a simple plan: the columns it reads outside its own rows
             // (whose x other ranks own), for the fused exchange
@@ -745,7 +758,8 @@ void bound_spmv(psc_bound* b, const double* x, double* y, cudaStream_t s) {
     } else if (b->canonical) {
         launch_spmv_parity(b->ro.as<int32_t>(), b->col.as<int32_t>(), b->val.as<double>(), x, y,
                            b->chunk_row.as<int4>(), b->n_chunks, b->item_seg.as<int2>(), b->long_list.as<int32_t>(),
-                           static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, b->spmv_short, b->rows(), s);
+                           static_cast<int>(b->long_rows), b->segs(), false, b->n_sms, b->spmv_short, b->rows(), s,
+                           nullptr, b->run_items.as<int4>(), b->n_run_items);
     } else {
         ck(cudaMemsetAsync(y, 0, static_cast<size_t>(b->rows()) * sizeof(double), s), "memset y");
         run_general(b, x, y, nullptr, nullptr, s);
@@ -1326,7 +1340,7 @@ PSC_API psc_status psc_bound_info(const psc_bound* b, int64_t out[8]) {
         require(b && out, "bound_info: null argument");
         out[0] = b->rows();
         out[1] = b->canonical ? b->n_segments : -1;
-        out[2] = b->kernel == PSC_KERNEL_SPMV ? b->n_chunks : b->n_blocks;
+        out[2] = b->kernel == PSC_KERNEL_SPMV ? (b->n_run_items > 0 ? b->n_run_items : b->n_chunks) : b->n_blocks;
         out[3] = !b->canonical ? 1 : b->fast_passes ? 2 : 0;
         out[4] = b->algorithmic_bytes();
         out[5] = b->device_bytes();

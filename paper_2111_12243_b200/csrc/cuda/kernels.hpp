@@ -90,7 +90,7 @@ void launch_spmv_parity(const int32_t* ro, const int32_t* col, const double* val
                         double* y, const int4* items, int n_items, const int2* item_seg,
                         const int32_t* long_rows, int n_long, SegmentsDev segs, bool accumulate, int n_sms,
                         int short_rows, int n_rows, cudaStream_t stream,
-                        const PeerDev* peer = nullptr);
+                        const PeerDev* peer = nullptr, const int4* run_items = nullptr, int n_run_items = 0);
 
 // Sync-free blocked record solve (kernels.cu sptrsv_rec_kernel): blocks of
 // rows (block_row: prefix sums of block sizes), solved by units listed in

@@ -613,6 +613,52 @@ bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows) {
     return true;
 }
 
+int64_t build_run_items(const Lowered& L, const psc_csr_view& a, std::vector<int32_t>& items) {
+    const int32_t nr = L.row_end - L.row_begin;
+    const int64_t kb = a.row_offsets[L.row_begin];
+    items.clear();
+    int64_t in_runs = 0;
+    auto emit = [&](int32_t r0, int32_t count, int32_t n) {  // local rows [r0, r0 + count)
+        const int64_t k0 = a.row_offsets[r0 + L.row_begin];
+        items.push_back(r0);
+        items.push_back(count);
+        items.push_back(static_cast<int32_t>(k0 - kb));
+        items.push_back(n);
+        for (int j = 0; j < 16; ++j) items.push_back(j < n ? a.col_indices[k0 + j] : 0);
+    };
+    int32_t loose0 = -1;  // open range of rows outside runs
+    auto flush_loose = [&](int32_t end) {
+        for (int32_t r = loose0; loose0 >= 0 && r < end; r += 32) emit(r, std::min<int32_t>(32, end - r), -1);
+        loose0 = -1;
+    };
+    int32_t r = 0;
+    while (r < nr) {
+        const int64_t k0 = a.row_offsets[r + L.row_begin];
+        const int32_t n = static_cast<int32_t>(a.row_offsets[r + L.row_begin + 1] - k0);
+        int32_t e = r + 1;
+        if (n >= 1 && n <= 16) {
+            while (e < nr) {
+                const int64_t ke = a.row_offsets[e + L.row_begin];
+                if (a.row_offsets[e + L.row_begin + 1] - ke != n) break;
+                bool same = true;
+                for (int32_t j = 0; j < n && same; ++j) same = a.col_indices[ke + j] == a.col_indices[k0 + j] + (e - r);
+                if (!same) break;
+                ++e;
+            }
+        }
+        if (e - r >= kRunMinRows) {
+            flush_loose(r);
+            for (int32_t q = r; q < e; q += 32) emit(q, std::min<int32_t>(32, e - q), n);
+            in_runs += e - r;
+        } else if (loose0 < 0) {
+            loose0 = r;
+        }
+        r = e;
+    }
+    flush_loose(nr);
+    return in_runs;
+}
+
 void block_halos(Lowered& L, const psc_csr_view& a) {
     const int32_t nb = static_cast<int32_t>(L.block_row.size()) - 1;
     const int32_t nr = L.row_end - L.row_begin;

@@ -114,6 +114,14 @@ bool tile_chain_blocks(Lowered& L, const psc_csr_view& a, int max_rows);
 // or tile_chain_blocks).
 void block_halos(Lowered& L, const psc_csr_view& a);
 
+// Warp items of the thread-per-row SpMV (simple plans whose rows hold <= 16 entries; kernels.cu
+// spmv_run_kernel), 20 ints each: {first local row, rows (<= 32), first local CSR position, n,
+// tmpl[16]}. n >= 0: a piece of a shifted run -- >= kRunMinRows consecutive rows of n entries each
+// whose columns are the first row's plus the row distance (tmpl = the item's first row's columns);
+// n = -1: consecutive rows outside such runs. Returns the rows covered by run items.
+constexpr int kRunMinRows = 16;
+int64_t build_run_items(const Lowered& L, const psc_csr_view& a, std::vector<int32_t>& items);
+
 // General-path lowering of a plan with explicit tables (imported with
 // psc_plan_from_arrays: the reference's own CodeletPlan) without a matrix:
 // Executor::run(plan, ctx) semantics (executor.hpp:45). Index ranges come

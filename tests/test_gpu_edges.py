@@ -77,6 +77,48 @@ def test_spmv_row_length_boundaries(exe, width):
     _spmv_check(exe, _csr(n, 6000, ent))
 
 
+@pytest.mark.parametrize("width", [1, 3, 4, 5, 7, 8, 9, 12, 13, 16])
+def test_spmv_shifted_runs(monkeypatch, width):
+    """Banded matrices of short rows: interior rows form shifted runs (the
+    same length, the columns of the row above plus one) and take
+    spmv_run_kernel's template path (no row offsets or column loads); rows
+    clipped by the matrix edge, rows that break a run, runs shorter than the
+    minimum, empty rows and a wide rectangular tail go through CSR in the same
+    kernel. Bitwise equal to the oracle through run_spmv and through the
+    bound device path, and to the row kernel (PSC_SPMV_RUNS=0)."""
+    import torch
+    n, n_cols = 1500, 1700
+    rng = np.random.default_rng(100 + width)
+    offs = sorted(set([0, 1, -1, 40, -40, 3, -3, 100, -7, 11, 23, -100, 57, -57, 150, 170][:width]))
+    ent = []
+    for r in range(n):
+        if 200 <= r < 215:
+            continue  # empty rows
+        if r % 97 == 5 or 300 <= r < 330 and r % 2:  # rows that break runs; runs of one row
+            cols = rng.choice(n_cols, size=rng.integers(1, min(16, width + 2) + 1), replace=False)
+        else:
+            cols = [r + o for o in offs if 0 <= r + o < n_cols]
+        ent += [(r, int(c), float(rng.uniform(-1, 1))) for c in cols]
+    a = _csr(n, n_cols, ent)
+    plan = P.inspect(KernelKind.Spmv, a, 3, 8)
+    x = P.uniform_vector(a.n_cols, 7)
+    want = Oracle.run_spmv(plan.export_arrays(), a.view(), x)
+    units = {}
+    for runs in ("1", "0"):
+        monkeypatch.setenv("PSC_SPMV_RUNS", runs)
+        exe = P.Executor(1)
+        y = np.full(a.n_rows, np.nan)
+        P.run_spmv(plan, a, x, y, exe)
+        assert bitwise_equal(y, want), (width, runs)
+        for mode in (0, 1):  # PSC_MODE_PARITY, PSC_MODE_FAST: one-pass short-row plans share the kernel
+            bound = P.BoundPlan(exe, plan, a, mode=mode)
+            yd = torch.full((a.n_rows,), float("nan"), dtype=torch.float64, device="cuda")
+            bound.spmv(torch.from_numpy(x).cuda(), yd)
+            assert bitwise_equal(yd.cpu().numpy(), want), (width, runs, mode)
+            units[runs] = bound.info()["work_units"]
+    assert units["1"] != units["0"]  # the run items were in use
+
+
 def test_sptrsv_tiny(exe):
     _sptrsv_check(exe, _csr(1, 1, [(0, 0, 3.0)]))
     _sptrsv_check(exe, _lower(50, lambda r: []))  # diagonal only
