@@ -1,6 +1,15 @@
-# config-4 solve: GPU tests, bench line (run under gpurun)
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 400 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.jsonl 2> gpurun_out/bench_c4.err
-python -c "
-import json; d=json.loads(open('gpurun_out/bench_c4.jsonl').read().strip().splitlines()[-1]); print('c4 ms', round(d['ms_per_step'],3), 'frac', round(d['roofline']['frac'],4))" || tail -3 gpurun_out/bench_c4.err
-timeout 500 python tools/trace_c4.py 1.0 2>&1 | tail -4
+#!/bin/bash
+# Config 4 (streaming SpTRSV): dense triangle phase on and off, and the solve tests.
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -x -q -m gpu -k "sptrsv or acceptance or configs or baselines or bound_device" > gpurun_out/c4_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/c4_pytest.log
+tail -5 gpurun_out/c4_pytest.log
+for d in 1 0; do
+  PSC_TRSV_DENSE=$d timeout 900 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_dense$d.jsonl 2> gpurun_out/c4_dense$d.err; echo "rc=$?"
+  python - <<PY
+import json
+for l in open("gpurun_out/c4_dense$d.jsonl"):
+    try: d=json.loads(l)
+    except Exception: continue
+    print("DENSE=$d", d.get("ms_per_step"), d.get("value"), d.get("roofline",{}).get("frac"))
+PY
+done
