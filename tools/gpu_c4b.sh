@@ -1,9 +1,7 @@
 #!/bin/bash
-# Config 4: buffers per L2 round (PSC_TRSV_BURST) A/B, after the solve tests with bursts on.
+# Config 4: buffers per L2 round (PSC_TRSV_BURST) A/B and the critical-path trace.
 mkdir -p gpurun_out
-PSC_TRSV_BURST=4 timeout 1200 python -m pytest tests -x -q -m gpu -k "sptrsv or acceptance or configs or baselines or bound_device" > gpurun_out/c4b_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/c4b_pytest.log
-tail -3 gpurun_out/c4b_pytest.log
-for b in 1 2 4 8 1 4; do
+for b in 8 16 64 8 16; do
   PSC_TRSV_BURST=$b timeout 900 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_burst$b.jsonl 2> gpurun_out/c4_burst$b.err
   python - <<PY
 import json
@@ -13,3 +11,4 @@ for l in open("gpurun_out/c4_burst$b.jsonl"):
     print("BURST=$b", d.get("ms_per_step"), d.get("roofline",{}).get("frac"))
 PY
 done
+timeout 900 python tools/trace_c4.py 1.0 2>&1 | tee gpurun_out/c4_trace_burst8.log | tail -8
