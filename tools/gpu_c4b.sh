@@ -2,14 +2,13 @@
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -x -q -m gpu -k "sptrsv or acceptance or configs or baselines or bound_device" > gpurun_out/c4b_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/c4b_pytest.log
 tail -3 gpurun_out/c4b_pytest.log
-for d in 1 0 1; do
-  PSC_TRSV_DENSE=$d timeout 900 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_d$d.jsonl 2> gpurun_out/c4_d$d.err
+for d in 1 0 1 0; do
+  PSC_TRSV_INCR=$d timeout 900 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_i$d.jsonl 2> gpurun_out/c4_i$d.err
   python - <<PY
 import json
-for l in open("gpurun_out/c4_d$d.jsonl"):
+for l in open("gpurun_out/c4_i$d.jsonl"):
     try: d=json.loads(l)
     except Exception: continue
-    print("DENSE=$d", d.get("ms_per_step"), d.get("roofline",{}).get("frac"))
+    print("INCR=$d", d.get("ms_per_step"), d.get("roofline",{}).get("frac"), str(d.get("parity"))[:30])
 PY
 done
-PSC_TRSV_TRACE_ROWS=0 timeout 900 python tools/trace_c4.py 1.0 2>&1 | tee gpurun_out/c4_trace_norows.log | tail -3
