@@ -301,12 +301,16 @@ def test_division_matches_ieee():
         assert bad.value == 0, (span, bad.value)
 
 
-@pytest.mark.parametrize("lean", ["2", "4"])
+@pytest.mark.parametrize("lean", ["2", "4", "4-generic-triangle"])
 @pytest.mark.parametrize("block_rows", ["1024", "0"])
 def test_sptrsv_round_kernels_bitwise(monkeypatch, lean, block_rows):
     """Both solve kernels (records where they apply, PSC_TRSV_LEAN=2; the
-    streaming / unit queue, 4), with default and small blocks (many operands
-    from earlier blocks), equal the oracle."""
+    streaming / unit queue, 4 -- with its dense triangle phase and with the
+    generic one only, PSC_TRSV_DENSE=0), with default and small blocks (many
+    operands from earlier blocks), equal the oracle."""
+    if lean.endswith("generic-triangle"):
+        monkeypatch.setenv("PSC_TRSV_DENSE", "0")
+        lean = "4"
     monkeypatch.setenv("PSC_TRSV_LEAN", lean)
     if block_rows != "0":
         monkeypatch.setenv("PSC_SPTRSV_BLOCK_ROWS", block_rows)
