@@ -345,6 +345,8 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
         // lengths and x offsets
         std::vector<int32_t> group_len(nr, 0);  // > 0 at a group's first row
         const char* gv = std::getenv("PSC_SPMV_GROUPS");
+        const char* sgv = std::getenv("PSC_SPMV_GROUP_SHIFT");
+        const bool shift_groups = !(sgv && sgv[0] == '0');
         if (!L.simple && !(gv && gv[0] == '0')) {
             auto templ = [&](int32_t r) {  // row r qualifies as a template
                 const int32_t q0 = L.row_seg_ptr[r], q1 = L.row_seg_ptr[r + 1];
@@ -370,8 +372,28 @@ Lowered lower_plan(const Plan& p, const psc_csr_view& a, int64_t part_begin, int
                     while (g < kGroupRows && r + g < nr && templ(r + g) && same(r, r + g)) ++g;
                 if (g >= 2) {
                     group_len[r] = g;
-                    const int32_t q0 = L.row_seg_ptr[r];
-                    L.groups.insert(L.groups.end(), {r, g, k_of(r), k_of(r + 1) - k_of(r), q0, L.row_seg_ptr[r + 1] - q0, 0, 0});
+                    const int32_t q0 = L.row_seg_ptr[r], S = L.row_seg_ptr[r + 1] - q0;
+                    const int32_t k0 = k_of(r), C = k_of(r + 1) - k0;
+                    // A group whose template is the previous group's shifted by a constant column
+                    // distance (the next node of a stencil line) takes its columns and segment
+                    // table from that group's template: {.., q0_t, S, k0_t, shift}; the line's
+                    // groups then read one template (L2-resident) instead of their own columns.
+                    int32_t qt = q0, kt = k0, shift = 0;
+                    if (shift_groups && !L.groups.empty()) {
+                        const int32_t* pg = L.groups.data() + L.groups.size() - 8;
+                        const int32_t pr = pg[0], pk = pg[2], pq = L.row_seg_ptr[pr];
+                        bool ok = pr + pg[1] == r && pg[3] == C && pg[5] == S;
+                        for (int32_t q = 0; q < S && ok; ++q) ok = L.seg_len[pq + q] == L.seg_len[q0 + q];
+                        const int64_t kb = L.k_begin;
+                        const int32_t d = ok ? a.col_indices[kb + k0] - a.col_indices[kb + pk] : 0;
+                        for (int32_t c = 0; c < C && ok; ++c) ok = a.col_indices[kb + k0 + c] == a.col_indices[kb + pk + c] + d;
+                        if (ok) {
+                            qt = pg[4];
+                            kt = pg[6];
+                            shift = pg[7] + d;
+                        }
+                    }
+                    L.groups.insert(L.groups.end(), {r, g, k0, C, qt, S, kt, shift});
                 }
                 r += g;
             }
