@@ -185,7 +185,7 @@ struct psc_bound {
                                 &g_kind, &g_m, &g_n, &g_form, &g_base, &g_so, &g_si, &g_tab, &g_tables, &g_frow,
                                 &g_fdiag, &g_frhs})
             t += b->bytes;
-        t += fp_carry_val.bytes + fp_carry_row.bytes;
+        t += fp_carry_val.bytes + fp_carry_row.bytes + run_items.bytes;
         for (int q = 0; q < kMaxSplitPasses; ++q)
             t += fl_colf[q].bytes + fl_val[q].bytes + fl_m0[q].bytes;
         return static_cast<int64_t>(t);
