@@ -511,10 +511,19 @@ def run_ours(args):
         "bound": info,
     }
     if kernel == "sptrsv":  # the solve is bound by its dependency chain
+        # a bitwise solve carries each x into the next level through 7 dependent FP64 operations
+        # (multiply, add, 0 + partial, subtract, three division steps, 8-9 cycles each) plus the hop
+        # between lanes: ~100 cycles per level at best
+        sm_ghz = float(line["clocks"].get("sm_max_mhz") or 1965.0) / 1e3
+        floor_ms = n_parts * 100.0 / sm_ghz * 1e-6
         line["roofline"]["critical_path"] = {
             "levels": n_parts, "ns_per_level": ms_step * 1e6 / max(1, n_parts),
-            "note": "sync-free solve: time ~ levels x per-level hop latency"}
-        line["roofline"]["record_pack"] = "the per-row record pack (trsv_pack_kernel) runs at bind and after a value change, outside the timed step"
+            "parity_floor_ms": floor_ms,
+            "target_0p30_ms": info["algorithmic_bytes"] / (0.30 * peak * 1e9) * 1e3,
+            "note": "sync-free solve: time ~ levels x per-level hop latency; parity_floor_ms = levels x ~100 cycles "
+                    "(the dependent FP64 chain of one row), the least any bitwise-equal solve can take"}
+        if args.config != 4:  # (config 4's long rows take the streaming kernel: no records)
+            line["roofline"]["record_pack"] = "the per-row record pack (trsv_pack_kernel) runs at bind and after a value change, outside the timed step"
     if args.config == 5 and mode == "fast":  # uniformly random columns: the gathers, not HBM, bound the step
         line["roofline"]["gather_bound"] = {
             "note": "each entry gathers one x value at a random column (config 5); the L1/L2 path serves ~1 such gather "
